@@ -1,0 +1,175 @@
+/*
+ * tarragon.h — C ABI of the B200-native Tarragon MoE-layer round trip.
+ *
+ * One call of tg_moe_layer() is one pass of the attention-worker (AW) ->
+ * expert-worker (EW) -> AW round trip of one MoE layer, as in
+ * PAPER.md §2.2.1 ("every data-parallel AW ... selects a subset of
+ * experts, sends token embeddings to the corresponding EWs, and waits until
+ * all selected experts return their outputs") through the Reconfigurable
+ * Forwarding Engine's expert_io path (§4.2):
+ *   gate (fp32 top-k)  ->  ERT resolve (masked EW -> shadow)  ->  permute
+ *   ->  dispatch exchange  ->  grouped SwiGLU expert FFN  ->  combine
+ *   exchange  ->  weighted unpermute.
+ * The operation computed is out[t] = sum_{e in TopK(t)} w_{t,e} FFN_e(x_t)
+ * (+ FFN_shared(x_t)) (§2.1); DESIGN.md §3 lists every reading
+ * of a point the paper leaves open.
+ *
+ * Processes and devices.  One process ("rank") per GPU; every rank is an AW
+ * shard (it owns a contiguous block of the global tokens, "each AW
+ * serving a disjoint subset of requests") and hosts zero or more logical EWs
+ * ("EWs ... partition expert FFNs across GPUs").  Dispatch and combine
+ * are one-sided stores into peer-mapped buffers over NVLink (P:739, P:865-867:
+ * point-to-point, no collective group membership per call).
+ *
+ * Conventions.
+ *   - All tensors are row-major and contiguous.  bf16 = IEEE bfloat16 bits.
+ *   - "device" pointers are CUDA device pointers on the ctx's device.
+ *   - Every call returns tg_status; on failure tg_last_error() describes it.
+ *   - Validation errors are synchronous and leave the ctx unchanged.
+ *   - CUDA errors are sticky: once TG_ERR_CUDA is returned the ctx must be
+ *     finalised.  A ctx is not thread-safe.
+ *   - There is no CPU fallback: with no usable sm_100a device tg_init()
+ *     returns TG_ERR_CUDA / TG_ERR_UNSUPPORTED (a host-only ctx, device = -1,
+ *     exists for validating tables and masks; its tg_moe_layer() returns
+ *     TG_ERR_UNSUPPORTED).
+ */
+#ifndef TARRAGON_H_
+#define TARRAGON_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tg_ctx tg_ctx; /* opaque; one per (rank, MoE layer) */
+
+typedef enum {
+  TG_OK = 0,
+  TG_ERR_INVALID = -1,        /* bad argument, shape or capacity */
+  TG_ERR_NO_ROUTE = -2,       /* some expert has no unmasked candidate */
+  TG_ERR_NOT_LOADED = -3,     /* a candidate (ew, slot) does not hold that expert */
+  TG_ERR_STALE_VERSION = -4,  /* route-table version <= current */
+  TG_ERR_CUDA = -5,           /* CUDA runtime/driver error or device timeout (sticky) */
+  TG_ERR_PEER = -6,           /* peer mapping / exchange error */
+  TG_ERR_OOM = -7,            /* device allocation failed */
+  TG_ERR_UNSUPPORTED = -8     /* host-only ctx, or a shape outside the supported set */
+} tg_status;
+
+/* Layer shape and placement.  Copied by tg_init; the caller may free it.
+ *   d_model, n_experts, top_k, d_ffn : d, E, k, F  (north_star SwiGLU)
+ *     d % 64 == 0, F % 64 == 0, 1 <= k <= min(E, 8), E <= 256.
+ *   d_ffn_shared  : merged shared-expert width (0 = none), % 64 == 0.
+ *   n_ews, ew_rank: W logical EWs; EW w lives on rank ew_rank[w] (W may
+ *                   exceed world: several EWs per GPU).  EWs of one rank get
+ *                   consecutive bank slots in ew order.
+ *   slots_per_ew  : expert slots per EW (primaries + shadows).
+ *   max_tokens_per_rank : capacity of x/out per call on each rank.       */
+typedef struct {
+  int d_model, n_experts, top_k, d_ffn;
+  int d_ffn_shared;
+  int n_ews;
+  const int32_t *ew_rank; /* [n_ews] */
+  int slots_per_ew;
+  int max_tokens_per_rank;
+} tg_config;
+
+/* Create a ctx on `cuda_device` (-1: host-only ctx for table/mask logic).
+ * Allocates the expert bank, receive/combine buffers and flags in HBM.
+ * Collective in the sense that every rank must create its ctx with the same
+ * config before tg_connect_peers().                                      */
+tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg_ctx **out);
+
+/* Peer bootstrap (world > 1).  tg_peer_handle_size() bytes per rank: the
+ * caller gathers every rank's handle (e.g. torch.distributed.all_gather) and
+ * passes them concatenated in rank order to tg_connect_peers(), which maps
+ * each peer's buffers for direct NVLink loads/stores.  world == 1 needs no
+ * connect call.                                                           */
+size_t tg_peer_handle_size(void);
+tg_status tg_get_peer_handle(tg_ctx *ctx, void *out);
+tg_status tg_connect_peers(tg_ctx *ctx, const void *all_handles);
+
+/* Router weights Wg [E][d] bf16 (host or device source; copied).  SPMD.   */
+tg_status tg_load_gate(tg_ctx *ctx, const void *wg, int src_on_device);
+
+/* Load expert `expert_id` into slot `slot` of EW `ew` (P:954 shadow experts:
+ * loading the same expert into another (ew, slot) creates a bit-identical
+ * shadow replica).  w1, w3: [F][d] bf16; w2: [d][F] bf16.  Only the rank
+ * hosting `ew` reads the weights (others may pass NULL); every rank records
+ * slot -> expert.  Synchronous.  SPMD.                                     */
+tg_status tg_load_experts(tg_ctx *ctx, int ew, int slot, int expert_id, const void *w1,
+                          const void *w3, const void *w2, int src_on_device);
+
+/* Merged shared expert (F_sh = d_ffn_shared): w1, w3 [F_sh][d]; w2 [d][F_sh].
+ * Replicated on every rank; added to the routed sum with weight 1.        */
+tg_status tg_load_shared(tg_ctx *ctx, const void *w1, const void *w3, const void *w2,
+                         int src_on_device);
+
+/* Expert Routing Table (§4.2): cand[e][c] = (ew, slot) for
+ * c < max_cands, primaries then shadows, (-1, -1) padding.  Accepted only
+ * if version > current version (else TG_ERR_STALE_VERSION, table ignored),
+ * every candidate (ew, slot) holds expert e (else TG_ERR_NOT_LOADED), and
+ * every expert has an unmasked candidate (else TG_ERR_NO_ROUTE).  Host-only;
+ * takes effect at the NEXT tg_moe_layer call, without re-initialisation.  */
+tg_status tg_set_route_table(tg_ctx *ctx, uint64_t version, const int32_t *cand, int max_cands);
+
+/* Fail-stop an EW (masked = 1) or let it rejoin (0) (§3.3,
+ * P:914-916 §5.1).  Always applied.  From the next tg_moe_layer on, the
+ * masked EW receives no rows and none of its memory is read; its experts are
+ * served by the first unmasked candidate (a shadow).  Returns TG_ERR_NO_ROUTE
+ * as a warning if some expert lost its last candidate; tg_moe_layer then
+ * fails with TG_ERR_NO_ROUTE (nothing launched) until the table or mask is
+ * fixed.  Host-only, O(E * max_cands).                                     */
+tg_status tg_mask_worker(tg_ctx *ctx, int ew, int masked);
+
+/* One MoE layer round trip (collective: every rank calls it, same order).
+ * x: device bf16 [n_tokens][d] (this rank's tokens); out: device bf16
+ * [n_tokens][d], must not alias x.  n_tokens <= max_tokens_per_rank (may be
+ * 0).  Enqueued on `stream` (cudaStream_t; NULL = legacy default stream);
+ * returns without synchronising.  x must stay valid until the stream passes
+ * the call.                                                                */
+tg_status tg_moe_layer(tg_ctx *ctx, const void *x, void *out, int n_tokens, void *stream);
+
+/* End-to-end form: x_host/out_host are pinned HOST buffers.  Enqueues the
+ * H2D copy of x, the layer and the D2H copy of out on `stream`.            */
+tg_status tg_moe_layer_host(tg_ctx *ctx, const void *x_host, void *out_host, int n_tokens,
+                            void *stream);
+
+/* Routing of the LAST call, for parity tests (device destination buffers,
+ * any may be NULL):  idx int32 [n][k] (ascending expert id), w fp32 [n][k],
+ * dst_rank / dst_slot (bank slot on that rank) / dst_pos (row in that rank's
+ * receive buffer) int32 [n][k], counts int32 [world][S_max] = rows per
+ * (rank, bank slot) summed over ALL source ranks.  Enqueued on stream.      */
+tg_status tg_get_routing(tg_ctx *ctx, int32_t *idx, float *w, int32_t *dst_rank,
+                         int32_t *dst_slot, int32_t *dst_pos, int32_t *counts, void *stream);
+
+/* S_max = max bank slots on any rank; bank slot of (ew, slot) on its rank. */
+int tg_max_slots(const tg_ctx *ctx);
+int tg_bank_slot(const tg_ctx *ctx, int ew, int slot);
+
+/* Cumulative rows routed to each (rank, bank slot) since tg_init, from this
+ * rank's tokens: int64 [world][S_max] host array.  Synchronises the device. */
+tg_status tg_get_stats(tg_ctx *ctx, int64_t *rows);
+
+/* Per-kernel CUDA-event timing of the following calls (on = 1).
+ * tg_get_kernel_times(ctx, ms, &n): synchronises on the last call and writes
+ * n (<= 8) durations in launch order: router, rank, dispatch, gemm, combine. */
+tg_status tg_set_profiling(tg_ctx *ctx, int on);
+tg_status tg_get_kernel_times(tg_ctx *ctx, float *ms, int *n);
+
+/* Kernel launches enqueued by the last tg_moe_layer call. */
+int tg_last_launch_count(const tg_ctx *ctx);
+
+/* Human-readable description of the last error on ctx (or of the last
+ * failed tg_init if ctx == NULL).  Never NULL.                             */
+const char *tg_last_error(const tg_ctx *ctx);
+
+/* Free everything (collective with world > 1: peers must not be inside a
+ * tg_moe_layer call).                                                      */
+tg_status tg_finalize(tg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TARRAGON_H_ */

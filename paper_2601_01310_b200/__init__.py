@@ -1,0 +1,301 @@
+"""Python binding of libtarragon.so (include/tarragon.h) — argument marshalling only.
+
+Every step of the MoE-layer round trip (gate, ERT resolve, permute, dispatch,
+expert FFN, combine) runs in the library's sm_100a kernels.  PyTorch supplies
+device memory, streams and (for world > 1) the process group that carries the
+peer-handle all-gather.  There is no CPU fallback: if the library is missing
+this module raises on import, and a ctx created without a GPU (device = -1)
+refuses to compute.
+
+Functions keep the C names (tg_init, tg_load_experts, tg_set_route_table,
+tg_mask_worker, tg_moe_layer, ...); ``MoELayer`` bundles them for one layer.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtarragon.so")
+
+TG_OK, TG_ERR_INVALID, TG_ERR_NO_ROUTE, TG_ERR_NOT_LOADED = 0, -1, -2, -3
+TG_ERR_STALE_VERSION, TG_ERR_CUDA, TG_ERR_PEER, TG_ERR_OOM, TG_ERR_UNSUPPORTED = -4, -5, -6, -7, -8
+STATUS = {0: "TG_OK", -1: "TG_ERR_INVALID", -2: "TG_ERR_NO_ROUTE", -3: "TG_ERR_NOT_LOADED",
+          -4: "TG_ERR_STALE_VERSION", -5: "TG_ERR_CUDA", -6: "TG_ERR_PEER", -7: "TG_ERR_OOM",
+          -8: "TG_ERR_UNSUPPORTED"}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2601_01310_b200.build` "
+                      "(there is no CPU fallback)")
+
+
+class tg_config(ctypes.Structure):
+    _fields_ = [("d_model", ctypes.c_int), ("n_experts", ctypes.c_int), ("top_k", ctypes.c_int),
+                ("d_ffn", ctypes.c_int), ("d_ffn_shared", ctypes.c_int), ("n_ews", ctypes.c_int),
+                ("ew_rank", ctypes.POINTER(ctypes.c_int32)), ("slots_per_ew", ctypes.c_int),
+                ("max_tokens_per_rank", ctypes.c_int)]
+
+
+_lib = ctypes.CDLL(LIB_PATH)
+_P, _I, _U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64
+_SIG = {
+    "tg_init": ([ctypes.POINTER(tg_config), _I, _I, _I, ctypes.POINTER(_P)], _I),
+    "tg_peer_handle_size": ([], ctypes.c_size_t),
+    "tg_get_peer_handle": ([_P, _P], _I),
+    "tg_connect_peers": ([_P, _P], _I),
+    "tg_load_gate": ([_P, _P, _I], _I),
+    "tg_load_experts": ([_P, _I, _I, _I, _P, _P, _P, _I], _I),
+    "tg_load_shared": ([_P, _P, _P, _P, _I], _I),
+    "tg_set_route_table": ([_P, _U64, _P, _I], _I),
+    "tg_mask_worker": ([_P, _I, _I], _I),
+    "tg_moe_layer": ([_P, _P, _P, _I, _P], _I),
+    "tg_moe_layer_host": ([_P, _P, _P, _I, _P], _I),
+    "tg_get_routing": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
+    "tg_max_slots": ([_P], _I),
+    "tg_bank_slot": ([_P, _I, _I], _I),
+    "tg_get_stats": ([_P, _P], _I),
+    "tg_set_profiling": ([_P, _I], _I),
+    "tg_get_kernel_times": ([_P, _P, ctypes.POINTER(_I)], _I),
+    "tg_last_launch_count": ([_P], _I),
+    "tg_last_error": ([_P], ctypes.c_char_p),
+    "tg_finalize": ([_P], _I),
+}
+for _n, (_a, _r) in _SIG.items():
+    _f = getattr(_lib, _n)
+    _f.argtypes, _f.restype = _a, _r
+
+EXPORTED = tuple(_SIG)
+
+
+class TarragonError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        assert t.is_contiguous(), "tensors passed to libtarragon must be contiguous"
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    return int(t)
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _check(ctx, rc: int, what: str, ok=(TG_OK,)):
+    if rc not in ok:
+        raise TarragonError(rc, f"{what}: {tg_last_error(ctx)}")
+    return rc
+
+
+# ----------------------------------------------------------------- C-name API
+
+def tg_last_error(ctx) -> str:
+    return _lib.tg_last_error(ctx).decode()
+
+
+def tg_init(d_model, n_experts, top_k, d_ffn, n_ews, ew_rank: Sequence[int], slots_per_ew,
+            max_tokens_per_rank, rank=0, world=1, device=None, d_ffn_shared=0):
+    """Create a ctx; device=None -> torch.cuda.current_device(); device=-1 -> host-only ctx."""
+    if device is None:
+        device = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    ew = (ctypes.c_int32 * len(ew_rank))(*ew_rank)
+    cfg = tg_config(d_model, n_experts, top_k, d_ffn, d_ffn_shared, len(ew_rank), ew, slots_per_ew,
+                    max_tokens_per_rank)
+    h = _P()
+    rc = _lib.tg_init(ctypes.byref(cfg), rank, world, device, ctypes.byref(h))
+    _check(None, rc, "tg_init")
+    return h
+
+
+def tg_peer_handle_size() -> int:
+    return _lib.tg_peer_handle_size()
+
+
+def tg_get_peer_handle(ctx) -> bytes:
+    buf = ctypes.create_string_buffer(tg_peer_handle_size())
+    _check(ctx, _lib.tg_get_peer_handle(ctx, buf), "tg_get_peer_handle")
+    return buf.raw
+
+
+def tg_connect_peers(ctx, handles: bytes):
+    _check(ctx, _lib.tg_connect_peers(ctx, handles), "tg_connect_peers")
+
+
+def tg_load_gate(ctx, wg: torch.Tensor):
+    _check(ctx, _lib.tg_load_gate(ctx, _ptr(wg), int(wg.is_cuda)), "tg_load_gate")
+
+
+def tg_load_experts(ctx, ew, slot, expert_id, w1, w3, w2):
+    on_dev = int(w1 is not None and isinstance(w1, torch.Tensor) and w1.is_cuda)
+    _check(ctx, _lib.tg_load_experts(ctx, ew, slot, expert_id, _ptr(w1), _ptr(w3), _ptr(w2), on_dev),
+           "tg_load_experts")
+
+
+def tg_load_shared(ctx, w1, w3, w2):
+    _check(ctx, _lib.tg_load_shared(ctx, _ptr(w1), _ptr(w3), _ptr(w2), int(w1.is_cuda)), "tg_load_shared")
+
+
+def tg_set_route_table(ctx, version: int, cand: np.ndarray) -> int:
+    """cand int32 [E, C, 2]; returns the status (raises only on INVALID)."""
+    cand = np.ascontiguousarray(cand, dtype=np.int32)
+    return _lib.tg_set_route_table(ctx, int(version), cand.ctypes.data, cand.shape[1])
+
+
+def tg_mask_worker(ctx, ew: int, masked: int = 1) -> int:
+    """Returns TG_OK or TG_ERR_NO_ROUTE (warning: mask applied, some expert unroutable)."""
+    rc = _lib.tg_mask_worker(ctx, ew, masked)
+    return _check(ctx, rc, "tg_mask_worker", ok=(TG_OK, TG_ERR_NO_ROUTE))
+
+
+def tg_moe_layer(ctx, x: torch.Tensor, out: torch.Tensor, stream=None) -> int:
+    n = x.shape[0] if x is not None else 0
+    return _lib.tg_moe_layer(ctx, _ptr(x), _ptr(out), n, _stream(stream))
+
+
+def tg_moe_layer_host(ctx, x_host: torch.Tensor, out_host: torch.Tensor, stream=None) -> int:
+    return _lib.tg_moe_layer_host(ctx, _ptr(x_host), _ptr(out_host), x_host.shape[0], _stream(stream))
+
+
+def tg_get_routing(ctx, n_tokens, k, world, S_max, device, stream=None):
+    idx = torch.empty(n_tokens, k, dtype=torch.int32, device=device)
+    w = torch.empty(n_tokens, k, dtype=torch.float32, device=device)
+    dr = torch.empty(n_tokens, k, dtype=torch.int32, device=device)
+    ds = torch.empty(n_tokens, k, dtype=torch.int32, device=device)
+    dp = torch.empty(n_tokens, k, dtype=torch.int32, device=device)
+    counts = torch.empty(world, S_max, dtype=torch.int32, device=device)
+    _check(ctx, _lib.tg_get_routing(ctx, _ptr(idx), _ptr(w), _ptr(dr), _ptr(ds), _ptr(dp), _ptr(counts),
+                                    _stream(stream)), "tg_get_routing")
+    return dict(idx=idx, w=w, dst_rank=dr, dst_slot=ds, dst_pos=dp, counts=counts)
+
+
+def tg_max_slots(ctx) -> int:
+    return _lib.tg_max_slots(ctx)
+
+
+def tg_bank_slot(ctx, ew, slot) -> int:
+    return _lib.tg_bank_slot(ctx, ew, slot)
+
+
+def tg_get_stats(ctx, world, S_max) -> np.ndarray:
+    rows = np.zeros((world, S_max), np.int64)
+    _check(ctx, _lib.tg_get_stats(ctx, rows.ctypes.data), "tg_get_stats")
+    return rows
+
+
+def tg_set_profiling(ctx, on=True):
+    _check(ctx, _lib.tg_set_profiling(ctx, int(on)), "tg_set_profiling")
+
+
+def tg_get_kernel_times(ctx):
+    ms = (ctypes.c_float * 8)()
+    n = _I(0)
+    _check(ctx, _lib.tg_get_kernel_times(ctx, ms, ctypes.byref(n)), "tg_get_kernel_times")
+    return [ms[i] for i in range(n.value)]
+
+
+def tg_last_launch_count(ctx) -> int:
+    return _lib.tg_last_launch_count(ctx)
+
+
+def tg_finalize(ctx):
+    if ctx:
+        _lib.tg_finalize(ctx)
+
+
+KERNEL_NAMES = ("router", "rank", "dispatch", "gemm", "combine")
+
+
+# ----------------------------------------------------------------- convenience
+
+class MoELayer:
+    """One MoE layer on this rank: ctx + weights + route table.
+
+    placement: object with n_ews, ew_rank, slots_per_ew, hosted[ew][slot], cand
+    (see workloads.make_placement).  weights: object with wg, w1, w3, w2 lists
+    (torch bf16, host or device) and optional shared = (w1s, w3s, w2s).
+    For world > 1 pass an initialised torch.distributed process group: the
+    peer handles are all-gathered through it.
+    """
+
+    def __init__(self, shape, placement, weights, max_tokens_per_rank, rank=0, world=1, device=None,
+                 group=None, version=1):
+        self.shape, self.pl = shape, placement
+        self.rank, self.world = rank, world
+        self.device = torch.cuda.current_device() if device is None else device
+        self.ctx = tg_init(shape.d, shape.E, shape.k, shape.F, placement.n_ews, placement.ew_rank,
+                           placement.slots_per_ew, max_tokens_per_rank, rank, world, self.device,
+                           d_ffn_shared=shape.F_sh)
+        if world > 1:
+            import torch.distributed as dist
+            h = tg_get_peer_handle(self.ctx)
+            t = torch.frombuffer(bytearray(h), dtype=torch.uint8).to(f"cuda:{self.device}")
+            outs = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(outs, t, group=group)
+            blob = b"".join(bytes(o.cpu().numpy().tobytes()) for o in outs)
+            tg_connect_peers(self.ctx, blob)
+            dist.barrier(group=group)
+        tg_load_gate(self.ctx, weights.wg.contiguous())
+        for ew in range(placement.n_ews):
+            local = placement.ew_rank[ew] == rank
+            for sl, e in enumerate(placement.hosted[ew]):
+                if e < 0:
+                    continue
+                if local:
+                    tg_load_experts(self.ctx, ew, sl, e, weights.w1[e].contiguous(), weights.w3[e].contiguous(),
+                                    weights.w2[e].contiguous())
+                else:
+                    tg_load_experts(self.ctx, ew, sl, e, None, None, None)
+        if shape.F_sh:
+            tg_load_shared(self.ctx, *(w.contiguous() for w in weights.shared))
+        self.version = 0
+        self.set_route_table(placement.cand, version)
+        self.S_max = tg_max_slots(self.ctx)
+
+    def set_route_table(self, cand, version=None):
+        version = self.version + 1 if version is None else version
+        rc = tg_set_route_table(self.ctx, version, cand)
+        if rc == TG_OK:
+            self.version = version
+        return rc
+
+    def mask_worker(self, ew, masked=1):
+        return tg_mask_worker(self.ctx, ew, masked)
+
+    def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty_like(x)
+        rc = tg_moe_layer(self.ctx, x, out, stream)
+        _check(self.ctx, rc, "tg_moe_layer")
+        return out
+
+    def routing(self, n_tokens, stream=None):
+        return tg_get_routing(self.ctx, n_tokens, self.shape.k, self.world, self.S_max,
+                              f"cuda:{self.device}", stream)
+
+    def stats(self):
+        return tg_get_stats(self.ctx, self.world, self.S_max)
+
+    def close(self):
+        tg_finalize(self.ctx)
+        self.ctx = None
+
+    def __del__(self):
+        try:
+            if self.ctx:
+                self.close()
+        except Exception:
+            pass

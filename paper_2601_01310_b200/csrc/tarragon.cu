@@ -1,0 +1,562 @@
+// tarragon.cu — host runtime of libtarragon.so: the C ABI of include/tarragon.h.
+//
+// Host-side state per ctx: the layer's expert bank (HBM), the Expert Routing
+// Table with its version and the EW mask (§4.2, §5.1), the
+// resolved expert -> (rank, bank slot) snapshot handed to the router kernel at
+// each call (so a table flip or a mask takes effect at the next call with no
+// re-initialisation), peer mappings of every rank's receive/combine buffers
+// (CUDA IPC over NVLink), and the per-call launch sequence GK1..GK5.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tarragon.h"
+#include "tg_internal.h"
+
+using namespace tg;
+
+namespace {
+
+thread_local std::string g_init_error = "no error";
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+struct tg_ctx {
+  // ---- config
+  int d, E, k, F, Fsh, W, spe, T_max;
+  int rank, world, device;
+  std::vector<int32_t> ew_rank, ew_base;  // per EW: rank, first bank slot on its rank
+  std::vector<int> S_of_rank;             // bank slots per rank
+  int S_max = 0, S_loc = 0, nkeys = 0;
+  int R_cap = 0, R_sh0 = 0, R_tot = 0, nsplit = 1;
+  // ---- routing state (host)
+  std::vector<int32_t> hosted;            // [W][spe] expert id, -1 empty
+  std::vector<int32_t> cand;              // [E][C][2]
+  int C = 0;
+  uint64_t version = 0;
+  bool have_table = false;
+  std::vector<uint8_t> mask;              // [W]
+  std::vector<int32_t> rkey;              // [E] resolved key or -1
+  bool no_route = true;
+  bool gate_loaded = false, shared_loaded = false;
+  // ---- device
+  bool host_only = true;
+  int n_sms = 148;
+  bf16 *bank_w1 = nullptr, *bank_w3 = nullptr, *bank_w2 = nullptr, *wg = nullptr;
+  bf16 *w1s = nullptr, *w3s = nullptr, *w2s = nullptr;
+  uint8_t *sym = nullptr;                 // own symmetric region
+  SymLayout L{};
+  uint8_t *peer[kMaxWorld] = {nullptr};
+  bool peer_opened[kMaxWorld] = {false};
+  void *scratch = nullptr;
+  CallArgs args{};
+  TmaMaps maps{};
+  int *err_host = nullptr, *err_dev = nullptr;
+  bf16 *x_stage = nullptr, *out_stage = nullptr;   // for tg_moe_layer_host
+  uint32_t epoch = 0;
+  int last_T = 0;
+  int last_launches = 0;
+  bool sticky = false;
+  // profiling
+  bool prof = false;
+  cudaEvent_t ev[8] = {nullptr};
+  int n_ev = 0;
+  std::string errmsg = "no error";
+};
+
+static tg_status fail(tg_ctx *c, tg_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->errmsg = buf; else g_init_error = buf;
+  if (c && s == TG_ERR_CUDA) c->sticky = true;
+  return s;
+}
+
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) return fail(c, TG_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                          \
+  } while (0)
+
+static tg_status check_sticky(tg_ctx *c) {
+  if (c->sticky) return TG_ERR_CUDA;
+  if (c->err_host && *reinterpret_cast<volatile int *>(c->err_host) != 0)
+    return fail(c, TG_ERR_CUDA, "device-side error code 0x%x (timeout or capacity)", *c->err_host);
+  return TG_OK;
+}
+
+// ------------------------------------------------------------------ resolve
+// First unmasked candidate ("first healthy").  key = rank*S_max+slot.
+static void resolve(tg_ctx *c) {
+  c->rkey.assign(c->E, -1);
+  c->no_route = !c->have_table;
+  if (!c->have_table) return;
+  for (int e = 0; e < c->E; ++e) {
+    for (int j = 0; j < c->C; ++j) {
+      int ew = c->cand[(e * c->C + j) * 2], sl = c->cand[(e * c->C + j) * 2 + 1];
+      if (ew < 0 || c->mask[ew]) continue;
+      c->rkey[e] = c->ew_rank[ew] * c->S_max + c->ew_base[ew] + sl;
+      break;
+    }
+    if (c->rkey[e] < 0) c->no_route = true;
+  }
+}
+
+static tg_status make_map(tg_ctx *c, CUtensorMap *m, void *base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(c, TG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, TG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%u",
+                                     (int)r, (unsigned long long)rows, (unsigned long long)cols, box_rows);
+  return TG_OK;
+}
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+extern "C" {
+
+tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg_ctx **out) {
+  tg_ctx *c = nullptr;
+  if (!cfg || !out) return fail(nullptr, TG_ERR_INVALID, "null config or out pointer");
+  *out = nullptr;
+  const int d = cfg->d_model, E = cfg->n_experts, k = cfg->top_k, F = cfg->d_ffn, Fsh = cfg->d_ffn_shared;
+  if (d <= 0 || d % 64 || F <= 0 || F % 64 || Fsh < 0 || Fsh % 64 || E < 1 || E > kMaxExperts || k < 1 ||
+      k > E || k > kMaxK)
+    return fail(nullptr, TG_ERR_INVALID, "shape: need d,F,F_sh %% 64 == 0, 1 <= k <= min(E,8), E <= 256 "
+                                         "(d=%d F=%d F_sh=%d E=%d k=%d)", d, F, Fsh, E, k);
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+    return fail(nullptr, TG_ERR_INVALID, "rank %d / world %d (world <= %d)", rank, world, kMaxWorld);
+  if (cfg->n_ews < 1 || !cfg->ew_rank || cfg->slots_per_ew < 1 || cfg->max_tokens_per_rank < 0)
+    return fail(nullptr, TG_ERR_INVALID, "placement: n_ews, ew_rank, slots_per_ew, max_tokens_per_rank");
+  c = new tg_ctx();
+  c->d = d; c->E = E; c->k = k; c->F = F; c->Fsh = Fsh;
+  c->W = cfg->n_ews; c->spe = cfg->slots_per_ew; c->T_max = cfg->max_tokens_per_rank;
+  c->rank = rank; c->world = world; c->device = cuda_device;
+  c->ew_rank.assign(cfg->ew_rank, cfg->ew_rank + c->W);
+  c->S_of_rank.assign(world, 0);
+  c->ew_base.resize(c->W);
+  for (int w = 0; w < c->W; ++w) {
+    int r = c->ew_rank[w];
+    if (r < 0 || r >= world) { delete c; return fail(nullptr, TG_ERR_INVALID, "ew_rank[%d] = %d out of range", w, r); }
+    c->ew_base[w] = c->S_of_rank[r];
+    c->S_of_rank[r] += c->spe;
+  }
+  for (int r = 0; r < world; ++r) c->S_max = std::max(c->S_max, c->S_of_rank[r]);
+  c->S_loc = c->S_of_rank[rank];
+  c->nkeys = world * c->S_max;
+  if (c->nkeys > kMaxKeys) { delete c; return fail(nullptr, TG_ERR_INVALID, "world * slots per rank = %d > %d", c->nkeys, kMaxKeys); }
+  c->hosted.assign((size_t)c->W * c->spe, -1);
+  c->mask.assign(c->W, 0);
+  c->rkey.assign(E, -1);
+  // worst-case rows received by one rank: every token of every rank, at most
+  // min(k, S_loc) rows each (distinct experts -> distinct slots)
+  c->R_cap = world * c->T_max * std::min(k, std::max(c->S_loc, 1));
+  c->R_sh0 = c->R_cap;
+  c->R_tot = c->R_cap + (Fsh > 0 ? c->T_max : 0);
+  // fixed split-K for long GEMM2 reductions: a function of the shape only
+  c->nsplit = (F / BK >= 128 && (F / BK) % 2 == 0) ? 2 : 1;
+  if (cuda_device < 0) { *out = c; return TG_OK; }
+
+  // ---------------------------------------------------------------- device
+  c->host_only = false;
+  auto bail = [&](tg_status s) { g_init_error = c->errmsg; tg_finalize(c); return s; };
+#define CKI(call)                                                                                 \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) {                                                                      \
+      fail(c, e_ == cudaErrorMemoryAllocation ? TG_ERR_OOM : TG_ERR_CUDA, "%s: %s", #call,        \
+           cudaGetErrorString(e_));                                                               \
+      return bail(e_ == cudaErrorMemoryAllocation ? TG_ERR_OOM : TG_ERR_CUDA);                    \
+    }                                                                                             \
+  } while (0)
+  CKI(cudaSetDevice(cuda_device));
+  cudaDeviceProp prop;
+  CKI(cudaGetDeviceProperties(&prop, cuda_device));
+  if (prop.major != 10) {
+    fail(c, TG_ERR_UNSUPPORTED, "device %d is sm_%d%d; libtarragon is built for sm_100a only", cuda_device,
+         prop.major, prop.minor);
+    return bail(TG_ERR_UNSUPPORTED);
+  }
+  c->n_sms = prop.multiProcessorCount;
+  const size_t S_loc = std::max(c->S_loc, 1);
+  CKI(cudaMalloc(&c->bank_w1, S_loc * F * d * 2));
+  CKI(cudaMalloc(&c->bank_w3, S_loc * F * d * 2));
+  CKI(cudaMalloc(&c->bank_w2, S_loc * F * d * 2));
+  CKI(cudaMalloc(&c->wg, (size_t)E * d * 2));
+  if (Fsh > 0) {
+    CKI(cudaMalloc(&c->w1s, (size_t)Fsh * d * 2));
+    CKI(cudaMalloc(&c->w3s, (size_t)Fsh * d * 2));
+    CKI(cudaMalloc(&c->w2s, (size_t)Fsh * d * 2));
+  }
+  // symmetric region
+  const size_t Tm = std::max(c->T_max, 1);
+  SymLayout &L = c->L;
+  size_t off = 0;
+  L.recv = off; off = align_up(off + (size_t)c->R_tot * d * 2, 1024);
+  L.meta = off; off = align_up(off + (size_t)c->R_tot * 8, 1024);
+  L.ybuf = off; off = align_up(off + Tm * k * d * 2, 1024);
+  L.cnt_all = off; off = align_up(off + (size_t)2 * world * c->nkeys * 4, 1024);
+  L.flags = off; off = align_up(off + 3 * kMaxWorld * 4, 1024);
+  L.total = off;
+  CKI(cudaMalloc(&c->sym, L.total));
+  CKI(cudaMemset(c->sym, 0, L.total));
+  c->peer[rank] = c->sym;
+  // local scratch
+  const int nblk_max = (int)((Tm + kRankBlock - 1) / kRankBlock);
+  const int ftiles = (F + BM - 1) / BM, ctiles = (d + BM - 1) / BM;
+  const int nt_max = (c->R_cap + BN_MAX - 1) / BN_MAX + (int)S_loc + 1;
+  const int ftiles_sh = Fsh > 0 ? (Fsh + BM - 1) / BM : 0;
+  const int nt_sh = (int)((Tm + BN_MAX - 1) / BN_MAX);
+  c->args.n_units_max = nt_max * (ftiles + ctiles * c->nsplit) + nt_sh * (ftiles_sh + ctiles) + 16;
+  c->args.n_ctr_max = nt_max * (1 + ctiles) + nt_sh + 16;
+  size_t so = 0;
+  auto carve = [&](size_t bytes) { size_t o = so; so = align_up(so + bytes, 256); return o; };
+  size_t o_idx = carve(Tm * k * 4), o_w = carve(Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
+  size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
+  size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
+  size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(64);
+  size_t o_ctr = carve((size_t)c->args.n_ctr_max * 4), o_units = carve((size_t)c->args.n_units_max * sizeof(Unit));
+  size_t o_nu = carve(16);
+  size_t o_H = carve((size_t)c->R_cap * F * 2);
+  size_t o_Hs = carve(Fsh > 0 ? Tm * Fsh * 2 : 0);
+  size_t o_ws = carve(c->nsplit > 1 ? (size_t)c->nsplit * c->R_cap * d * 4 : 0);
+  size_t o_ysh = carve(Fsh > 0 ? Tm * d * 2 : 0);
+  size_t o_xs = carve(Tm * d * 2), o_os = carve(Tm * d * 2);
+  CKI(cudaMalloc(&c->scratch, so));
+  CKI(cudaMemset(c->scratch, 0, so));
+  uint8_t *sb = reinterpret_cast<uint8_t *>(c->scratch);
+  CallArgs &a = c->args;
+  a.d = d; a.E = E; a.k = k; a.F = F; a.Fsh = Fsh; a.world = world; a.rank = rank;
+  a.S_max = c->S_max; a.S_loc = c->S_loc; a.nkeys = c->nkeys; a.T_max = c->T_max; a.R_cap = c->R_cap;
+  a.R_sh0 = c->R_sh0; a.nsplit = c->nsplit;
+  a.wg = c->wg;
+  a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.key = (int32_t *)(sb + o_key);
+  a.lrank = (int32_t *)(sb + o_lrank); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
+  a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
+  a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
+  a.sync = (int32_t *)(sb + o_sync); a.ctr = (int32_t *)(sb + o_ctr); a.units = (Unit *)(sb + o_units);
+  a.n_units = (int32_t *)(sb + o_nu);
+  a.H = (bf16 *)(sb + o_H); a.Hs = Fsh > 0 ? (bf16 *)(sb + o_Hs) : nullptr;
+  a.ws = c->nsplit > 1 ? (float *)(sb + o_ws) : nullptr; a.ysh = Fsh > 0 ? (bf16 *)(sb + o_ysh) : nullptr;
+  c->x_stage = (bf16 *)(sb + o_xs); c->out_stage = (bf16 *)(sb + o_os);
+  a.L = L;
+  CKI(cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
+  *c->err_host = 0;
+  CKI(cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
+  a.err = c->err_dev;
+  // tensor maps (fixed addresses)
+  tg_status s;
+  if ((s = make_map(c, &c->maps.w1, c->bank_w1, S_loc * F, d, BM)) != TG_OK) return bail(s);
+  if ((s = make_map(c, &c->maps.w3, c->bank_w3, S_loc * F, d, BM)) != TG_OK) return bail(s);
+  if ((s = make_map(c, &c->maps.w2, c->bank_w2, S_loc * d, F, BM)) != TG_OK) return bail(s);
+  if (Fsh > 0) {
+    if ((s = make_map(c, &c->maps.w1s, c->w1s, Fsh, d, BM)) != TG_OK) return bail(s);
+    if ((s = make_map(c, &c->maps.w3s, c->w3s, Fsh, d, BM)) != TG_OK) return bail(s);
+    if ((s = make_map(c, &c->maps.w2s, c->w2s, d, Fsh, BM)) != TG_OK) return bail(s);
+  } else {
+    c->maps.w1s = c->maps.w1; c->maps.w3s = c->maps.w3; c->maps.w2s = c->maps.w2;
+  }
+  for (int i = 0; i < kNumBoxes; ++i) {
+    uint32_t br = 16 * (i + 1);
+    if ((s = make_map(c, &c->maps.x[i], c->sym + L.recv, c->R_tot, d, br)) != TG_OK) return bail(s);
+    if ((s = make_map(c, &c->maps.h[i], a.H, std::max(c->R_cap, 1), F, br)) != TG_OK) return bail(s);
+    if (Fsh > 0) {
+      if ((s = make_map(c, &c->maps.hs[i], a.Hs, Tm, Fsh, br)) != TG_OK) return bail(s);
+    } else {
+      c->maps.hs[i] = c->maps.h[i];
+    }
+  }
+  CKI(gemm_configure());
+  for (int i = 0; i < 8; ++i) CKI(cudaEventCreate(&c->ev[i]));
+  CKI(cudaDeviceSynchronize());
+#undef CKI
+  *out = c;
+  return TG_OK;
+}
+
+size_t tg_peer_handle_size(void) { return sizeof(cudaIpcMemHandle_t); }
+
+tg_status tg_get_peer_handle(tg_ctx *c, void *out) {
+  if (!c || !out) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx has no device buffers");
+  CK(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->sym));
+  memcpy(out, &h, sizeof h);
+  return TG_OK;
+}
+
+tg_status tg_connect_peers(tg_ctx *c, const void *all) {
+  if (!c || !all) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx has no device buffers");
+  CK(cudaSetDevice(c->device));
+  const uint8_t *p = reinterpret_cast<const uint8_t *>(all);
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, p + (size_t)q * sizeof h, sizeof h);
+    void *ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(c, TG_ERR_PEER, "cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
+    c->peer[q] = reinterpret_cast<uint8_t *>(ptr);
+    c->peer_opened[q] = true;
+  }
+  return TG_OK;
+}
+
+static tg_status copy_in(tg_ctx *c, void *dst, const void *src, size_t bytes, int on_dev) {
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpy(dst, src, bytes, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  return TG_OK;
+}
+
+tg_status tg_load_gate(tg_ctx *c, const void *wg, int on_dev) {
+  if (!c || !wg) return TG_ERR_INVALID;
+  if (!c->host_only) {
+    tg_status s = copy_in(c, c->wg, wg, (size_t)c->E * c->d * 2, on_dev);
+    if (s) return s;
+  }
+  c->gate_loaded = true;
+  return TG_OK;
+}
+
+tg_status tg_load_experts(tg_ctx *c, int ew, int slot, int expert, const void *w1, const void *w3, const void *w2,
+                          int on_dev) {
+  if (!c) return TG_ERR_INVALID;
+  if (ew < 0 || ew >= c->W || slot < 0 || slot >= c->spe || expert < 0 || expert >= c->E)
+    return fail(c, TG_ERR_INVALID, "tg_load_experts: ew %d slot %d expert %d out of range", ew, slot, expert);
+  if (!c->host_only && c->ew_rank[ew] == c->rank) {
+    if (!w1 || !w3 || !w2) return fail(c, TG_ERR_INVALID, "tg_load_experts: null weights for a local EW");
+    const size_t b = (size_t)c->F * c->d * 2;
+    const size_t bs = (size_t)(c->ew_base[ew] + slot);
+    tg_status s;
+    if ((s = copy_in(c, reinterpret_cast<uint8_t *>(c->bank_w1) + bs * b, w1, b, on_dev))) return s;
+    if ((s = copy_in(c, reinterpret_cast<uint8_t *>(c->bank_w3) + bs * b, w3, b, on_dev))) return s;
+    if ((s = copy_in(c, reinterpret_cast<uint8_t *>(c->bank_w2) + bs * b, w2, b, on_dev))) return s;
+  }
+  c->hosted[(size_t)ew * c->spe + slot] = expert;
+  return TG_OK;
+}
+
+tg_status tg_load_shared(tg_ctx *c, const void *w1, const void *w3, const void *w2, int on_dev) {
+  if (!c || !w1 || !w3 || !w2) return TG_ERR_INVALID;
+  if (c->Fsh == 0) return fail(c, TG_ERR_INVALID, "config has no shared expert (d_ffn_shared = 0)");
+  if (!c->host_only) {
+    const size_t b = (size_t)c->Fsh * c->d * 2;
+    tg_status s;
+    if ((s = copy_in(c, c->w1s, w1, b, on_dev))) return s;
+    if ((s = copy_in(c, c->w3s, w3, b, on_dev))) return s;
+    if ((s = copy_in(c, c->w2s, w2, b, on_dev))) return s;
+  }
+  c->shared_loaded = true;
+  return TG_OK;
+}
+
+tg_status tg_set_route_table(tg_ctx *c, uint64_t version, const int32_t *cand, int C) {
+  if (!c || !cand || C < 1) return TG_ERR_INVALID;
+  if (c->have_table && version <= c->version)
+    return fail(c, TG_ERR_STALE_VERSION, "route table version %llu <= current %llu (ignored)",
+                (unsigned long long)version, (unsigned long long)c->version);
+  for (int e = 0; e < c->E; ++e)
+    for (int j = 0; j < C; ++j) {
+      int ew = cand[(e * C + j) * 2], sl = cand[(e * C + j) * 2 + 1];
+      if (ew < 0) continue;
+      if (ew >= c->W || sl < 0 || sl >= c->spe)
+        return fail(c, TG_ERR_INVALID, "candidate (%d, %d) of expert %d out of range", ew, sl, e);
+      if (c->hosted[(size_t)ew * c->spe + sl] != e)
+        return fail(c, TG_ERR_NOT_LOADED, "candidate (ew %d, slot %d) of expert %d holds expert %d", ew, sl, e,
+                    c->hosted[(size_t)ew * c->spe + sl]);
+    }
+  // routable under the current mask?
+  for (int e = 0; e < c->E; ++e) {
+    bool ok = false;
+    for (int j = 0; j < C && !ok; ++j) {
+      int ew = cand[(e * C + j) * 2];
+      ok = ew >= 0 && !c->mask[ew];
+    }
+    if (!ok) return fail(c, TG_ERR_NO_ROUTE, "expert %d has no unmasked candidate in the new table", e);
+  }
+  c->cand.assign(cand, cand + (size_t)c->E * C * 2);
+  c->C = C;
+  c->version = version;
+  c->have_table = true;
+  resolve(c);
+  return TG_OK;
+}
+
+tg_status tg_mask_worker(tg_ctx *c, int ew, int masked) {
+  if (!c) return TG_ERR_INVALID;
+  if (ew < 0 || ew >= c->W) return fail(c, TG_ERR_INVALID, "ew %d out of range", ew);
+  c->mask[ew] = masked ? 1 : 0;
+  resolve(c);
+  if (c->have_table && c->no_route) {
+    int e = 0;
+    while (e < c->E && c->rkey[e] >= 0) ++e;
+    return fail(c, TG_ERR_NO_ROUTE, "expert %d lost its last unmasked candidate", e);
+  }
+  return TG_OK;
+}
+
+int tg_max_slots(const tg_ctx *c) { return c ? c->S_max : -1; }
+int tg_bank_slot(const tg_ctx *c, int ew, int slot) {
+  if (!c || ew < 0 || ew >= c->W || slot < 0 || slot >= c->spe) return -1;
+  return c->ew_base[ew] + slot;
+}
+
+static void rec(tg_ctx *c, cudaStream_t s) {
+  if (c->prof && c->n_ev < 8) cudaEventRecord(c->ev[c->n_ev++], s);
+}
+
+tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream) {
+  if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device): no compute path");
+  tg_status st = check_sticky(c);
+  if (st) return st;
+  if (T < 0 || T > c->T_max) return fail(c, TG_ERR_INVALID, "n_tokens %d > max_tokens_per_rank %d", T, c->T_max);
+  if (T > 0 && (!x || !out)) return fail(c, TG_ERR_INVALID, "null x/out");
+  if (T > 0 && x == out) return fail(c, TG_ERR_INVALID, "out aliases x");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(c, TG_ERR_INVALID, "x/out must be 16-byte aligned");
+  if (!c->gate_loaded) return fail(c, TG_ERR_NOT_LOADED, "router weights not loaded (tg_load_gate)");
+  if (c->Fsh > 0 && !c->shared_loaded) return fail(c, TG_ERR_NOT_LOADED, "shared expert not loaded");
+  if (!c->have_table) return fail(c, TG_ERR_NOT_LOADED, "no route table (tg_set_route_table)");
+  if (c->no_route) return fail(c, TG_ERR_NO_ROUTE, "some expert has no unmasked candidate: nothing launched");
+  for (int q = 0; q < c->world; ++q)
+    if (!c->peer[q]) return fail(c, TG_ERR_PEER, "peer %d not connected (tg_connect_peers)", q);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  RouteKeys rk;
+  for (int e = 0; e < kMaxExperts; ++e) rk.key[e] = e < c->E ? c->rkey[e] : -1;
+  CallArgs a = c->args;
+  a.T = T;
+  a.x = reinterpret_cast<const bf16 *>(x);
+  a.out = reinterpret_cast<bf16 *>(out);
+  a.epoch = ++c->epoch;
+  for (int q = 0; q < kMaxWorld; ++q) a.sym[q] = q < c->world ? c->peer[q] : nullptr;
+  c->n_ev = 0;
+  rec(c, s);
+  CK(launch_router(a, rk, s));
+  rec(c, s);
+  CK(launch_rank(a, s));
+  rec(c, s);
+  CK(launch_dispatch(a, s));
+  rec(c, s);
+  CK(launch_gemm(a, c->maps, c->n_sms, s));
+  rec(c, s);
+  CK(launch_combine(a, s));
+  rec(c, s);
+  c->last_T = T;
+  c->last_launches = (T > 0 ? 1 : 0) + 4;
+  return TG_OK;
+}
+
+tg_status tg_moe_layer_host(tg_ctx *c, const void *xh, void *oh, int T, void *stream) {
+  if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device): no compute path");
+  if (T < 0 || T > c->T_max) return fail(c, TG_ERR_INVALID, "n_tokens %d > max_tokens_per_rank %d", T, c->T_max);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  const size_t b = (size_t)T * c->d * 2;
+  if (T > 0) CK(cudaMemcpyAsync(c->x_stage, xh, b, cudaMemcpyHostToDevice, s));
+  tg_status st = tg_moe_layer(c, c->x_stage, c->out_stage, T, stream);
+  if (st) return st;
+  if (T > 0) CK(cudaMemcpyAsync(oh, c->out_stage, b, cudaMemcpyDeviceToHost, s));
+  return TG_OK;
+}
+
+tg_status tg_get_routing(tg_ctx *c, int32_t *idx, float *w, int32_t *dst_rank, int32_t *dst_slot, int32_t *dst_pos,
+                         int32_t *counts, void *stream) {
+  if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  const size_t n = (size_t)c->last_T * c->k;
+  if (idx && n) CK(cudaMemcpyAsync(idx, c->args.idx, n * 4, cudaMemcpyDeviceToDevice, s));
+  if (w && n) CK(cudaMemcpyAsync(w, c->args.w, n * 4, cudaMemcpyDeviceToDevice, s));
+  if (dst_pos && n) CK(cudaMemcpyAsync(dst_pos, c->args.dst_pos, n * 4, cudaMemcpyDeviceToDevice, s));
+  if (counts) CK(cudaMemcpyAsync(counts, c->args.gcounts, (size_t)c->nkeys * 4, cudaMemcpyDeviceToDevice, s));
+  if ((dst_rank || dst_slot) && n) CK(launch_export_keys(c->args, (int)n, dst_rank, dst_slot, s));
+  return TG_OK;
+}
+
+tg_status tg_get_stats(tg_ctx *c, int64_t *rows) {
+  if (!c || !rows) return TG_ERR_INVALID;
+  if (c->host_only) {
+    memset(rows, 0, sizeof(int64_t) * c->nkeys);
+    return TG_OK;
+  }
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(rows, c->args.stats, sizeof(int64_t) * c->nkeys, cudaMemcpyDeviceToHost));
+  return check_sticky(c);
+}
+
+tg_status tg_set_profiling(tg_ctx *c, int on) {
+  if (!c) return TG_ERR_INVALID;
+  c->prof = on != 0;
+  return TG_OK;
+}
+
+tg_status tg_get_kernel_times(tg_ctx *c, float *ms, int *n) {
+  if (!c || !ms || !n) return TG_ERR_INVALID;
+  if (!c->prof || c->n_ev < 2) { *n = 0; return TG_OK; }
+  CK(cudaEventSynchronize(c->ev[c->n_ev - 1]));
+  for (int i = 0; i + 1 < c->n_ev; ++i) CK(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
+  *n = c->n_ev - 1;
+  return check_sticky(c);
+}
+
+int tg_last_launch_count(const tg_ctx *c) { return c ? c->last_launches : 0; }
+
+const char *tg_last_error(const tg_ctx *c) { return c ? c->errmsg.c_str() : g_init_error.c_str(); }
+
+tg_status tg_finalize(tg_ctx *c) {
+  if (!c) return TG_OK;
+  if (!c->host_only) {
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (int q = 0; q < kMaxWorld; ++q)
+      if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer[q]);
+    cudaFree(c->bank_w1); cudaFree(c->bank_w3); cudaFree(c->bank_w2); cudaFree(c->wg);
+    cudaFree(c->w1s); cudaFree(c->w3s); cudaFree(c->w2s);
+    cudaFree(c->sym); cudaFree(c->scratch);
+    if (c->err_host) cudaFreeHost(c->err_host);
+    for (int i = 0; i < 8; ++i) if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  }
+  delete c;
+  return TG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// tg_internal.h — device-side data layout shared by the host runtime and the
+// kernels of libtarragon.so.  Not part of the C ABI (include/tarragon.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tg {
+
+typedef __nv_bfloat16 bf16;
+
+constexpr int kMaxWorld = 8;
+constexpr int kMaxExperts = 256;
+constexpr int kMaxK = 8;
+constexpr int kMaxKeys = 1024;      // world * S_max  (key = rank * S_max + bank slot)
+constexpr int kRankBlock = 256;     // tokens per block of the rank kernel
+constexpr int kNumBoxes = 8;        // token-tile heights 16, 32, ..., 128
+
+// GEMM tiling: swap-AB, weights fill UMMA M = 128,
+// tokens are UMMA N (16..128), K staged 64 wide (one 128-B swizzle row).
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int BN_MAX = 128;
+constexpr int kStages = 4;
+constexpr int kTileBytes = 16384;               // 128 rows x 128 B
+constexpr int kStageBytes = 3 * kTileBytes;     // A0 (W1|W2), A1 (W3), B (X|H)
+constexpr int kSchedDepth = 8;
+constexpr int kGemmThreads = 256;               // w0 TMA, w1 MMA, w2 TMEM, w4-7 epilogue
+constexpr int kTmemCols = 512;                  // 2 accumulator buffers x 256 columns
+
+// Resolved ERT snapshot, passed by value to the router (host-resolved per
+// table/mask change): key[e] = rank * S_max + bank_slot.
+struct RouteKeys {
+  int32_t key[kMaxExperts];
+};
+
+enum UnitKind : int32_t { U_G1 = 0, U_G2 = 1, U_G1_SH = 2, U_G2_SH = 3 };
+
+// One GEMM work unit: a 128-row weight tile x up to 128 token rows of one slot.
+struct Unit {
+  int32_t kind;    // UnitKind
+  int32_t slot;    // local bank slot (routed) / 0 (shared)
+  int32_t m0;      // first weight row of the tile (f for GEMM1, c for GEMM2)
+  int32_t n0;      // first row in recv / H
+  int32_t nrows;   // token rows in this tile (1..128)
+  int32_t kb0;     // first 64-wide K block
+  int32_t kb1;     // one past the last K block
+  int32_t dep;     // GEMM1: counter to bump when done; GEMM2: counter to wait on
+  int32_t red;     // GEMM2 split-K: reduction counter (-1 if no split)
+  int32_t split;   // split index
+  int32_t nsplit;  // number of splits
+  int32_t dep_target;
+};
+
+struct TmaMaps {
+  CUtensorMap w1, w3, w2;          // expert bank
+  CUtensorMap w1s, w3s, w2s;       // shared expert
+  CUtensorMap x[kNumBoxes];        // receive buffer, box rows 16*(i+1)
+  CUtensorMap h[kNumBoxes];        // SwiGLU activations H, box rows 16*(i+1)
+  CUtensorMap hs[kNumBoxes];       // shared-expert activations
+};
+
+// Peer-visible ("symmetric") region: same layout and size on every rank, one
+// CUDA IPC handle per rank.  Offsets in bytes.
+struct SymLayout {
+  size_t recv;      // bf16 [R_cap][d]            dispatched token rows
+  size_t meta;      // int2 [R_cap]               origin (src rank, t*k + j)
+  size_t ybuf;      // bf16 [T_max][k][d]         expert outputs returned to this AW
+  size_t cnt_all;   // int32 [2][world][nkeys]    all-gathered per-source counts
+  size_t flags;     // uint32 [3][kMaxWorld]      cnt / data / comb epoch flags
+  size_t total;
+};
+constexpr int FLAG_CNT = 0, FLAG_DATA = 1, FLAG_COMB = 2;
+
+// Everything a call needs, by value (kernel parameter).
+struct CallArgs {
+  // shape
+  int d, E, k, F, Fsh, world, rank, S_max, S_loc, nkeys, T_max, R_cap, R_sh0, nsplit;
+  int T;                 // tokens on this rank for this call
+  uint32_t epoch;
+  // inputs / outputs
+  const bf16 *x;
+  bf16 *out;
+  const bf16 *wg;
+  // per-call scratch (local)
+  int32_t *idx;          // [T_max][k]
+  float *w;              // [T_max][k]
+  int32_t *key;          // [T_max][k] destination key of each pair
+  int32_t *lrank;        // [T_max][k] rank of the pair within its block and key
+  int32_t *bcnt;         // [nblk_max][nkeys] per-block counts -> exclusive block bases
+  int32_t *dbase;        // [nkeys] base row of this source in each (rank, slot)
+  int32_t *dst_pos;      // [T_max][k]
+  int32_t *gcounts;      // [nkeys] rows per (rank, slot) over all sources
+  int32_t *need_src;     // [kMaxWorld] source sends rows to this rank
+  int32_t *sent_to;      // [kMaxWorld] this rank sends rows to dest
+  int32_t *slot_rows;    // [S_loc] M_s on this rank
+  int64_t *stats;        // [nkeys]
+  int32_t *sync;         // [8] block/CTA done counters and scheduler
+  int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters
+  int n_ctr_max;
+  Unit *units;           // [n_units_max]
+  int32_t *n_units;      // [1]
+  int n_units_max;
+  int *err;              // host-mapped error word
+  // GEMM buffers (local)
+  bf16 *H;               // [R_cap][F]
+  bf16 *Hs;              // [T_max][Fsh]
+  float *ws;             // [nsplit][R_cap][d] split-K partials
+  bf16 *ysh;             // [T_max][d] shared-expert output
+  // symmetric region, own + peers
+  uint8_t *sym[kMaxWorld];
+  SymLayout L;
+};
+
+// Kernel launchers (tg_kernels.cu / tg_gemm.cu).  Return cudaGetLastError().
+cudaError_t launch_router(const CallArgs &a, const RouteKeys &rk, cudaStream_t s);
+cudaError_t launch_rank(const CallArgs &a, cudaStream_t s);
+cudaError_t launch_dispatch(const CallArgs &a, cudaStream_t s);
+cudaError_t launch_gemm(const CallArgs &a, const TmaMaps &maps, int n_sms, cudaStream_t s);
+cudaError_t launch_combine(const CallArgs &a, cudaStream_t s);
+cudaError_t launch_export_keys(const CallArgs &a, int n, int32_t *dst_rank, int32_t *dst_slot, cudaStream_t s);
+cudaError_t gemm_configure();
+size_t gemm_smem_bytes();
+
+}  // namespace tg

@@ -1,0 +1,69 @@
+"""Helpers for GPU-vs-oracle parity tests (test infrastructure)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+import workloads as wl
+
+NEAR_TIE = 1e-5       # north_star: k-th vs (k+1)-th logit gap below which routing may differ
+W_TOL = 1e-6          # |w_gpu - w_oracle|
+OUT_TOL = 2e-2        # max|out_gpu - out_oracle| <= OUT_TOL * RMS(out_oracle)  (north_star)
+
+
+def bf16_to_f64(u16: np.ndarray) -> np.ndarray:
+    return (u16.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def host_weights(L: wl.Layer):
+    w1 = [wl.as_u16(a) for a in L.w1]
+    w3 = [wl.as_u16(a) for a in L.w3]
+    w2 = [wl.as_u16(a) for a in L.w2]
+    sh = tuple(wl.as_u16(a) for a in L.shared) if L.shared is not None else None
+    return w1, w3, w2, sh
+
+
+def oracle_layer(L: wl.Layer, x: torch.Tensor, pl: wl.Placement, mask, G: int, tokens=None, n_threads=1):
+    w1, w3, w2, sh = host_weights(L)
+    return oracle.layer(wl.as_u16(x), wl.as_u16(L.wg), L.shape.k, w1, w3, w2, pl.cand, pl.ew_rank,
+                        pl.slots_per_ew, np.asarray(mask, np.uint8), G, shared=sh, tokens=tokens,
+                        n_threads=n_threads)
+
+
+def compare(ref: dict, gpu_out: np.ndarray, routing: dict, tokens=None, check_perm=True):
+    """Apply the parity criteria P1-P4; returns a report dict, asserts on failure."""
+    rep = {}
+    gap = ref["gap"]
+    near = gap < NEAR_TIE
+    rep["near_ties"] = int(near.sum())
+    idx_g = routing["idx"].cpu().numpy()
+    w_g = routing["w"].cpu().numpy()
+    ok = ~near
+    # P1 routing indices bit-exact except near ties
+    bad = np.any(idx_g != ref["idx"], axis=1) & ok
+    assert not bad.any(), f"P1: idx mismatch on {int(bad.sum())} non-near-tie tokens, first {np.nonzero(bad)[0][:5]}"
+    # P3 gate weights
+    same = np.all(idx_g == ref["idx"], axis=1)
+    dw = np.abs(w_g.astype(np.float64) - ref["w"].astype(np.float64))[same]
+    rep["max_dw"] = float(dw.max()) if dw.size else 0.0
+    assert rep["max_dw"] <= W_TOL, f"P3: max |dw| = {rep['max_dw']}"
+    # P2 permutation bit-exact (only meaningful when no near-tie token changed its set)
+    if check_perm and rep["near_ties"] == 0:
+        for kk in ("dst_rank", "dst_slot", "dst_pos"):
+            g = routing[kk].cpu().numpy()
+            assert np.array_equal(g, ref[kk]), f"P2: {kk} mismatch at {np.argwhere(g != ref[kk])[:5].tolist()}"
+        cg = routing["counts"].cpu().numpy()
+        assert np.array_equal(cg, ref["counts"]), "P2: counts mismatch"
+    # P4 outputs
+    out_ref = bf16_to_f64(ref["out"])
+    sel = ok if tokens is None else ok[tokens]
+    gpu = bf16_to_f64(gpu_out)
+    err = np.abs(gpu - out_ref)[sel]
+    rms = float(np.sqrt(np.mean(out_ref[sel] ** 2))) if sel.any() else 1.0
+    rep["rms"] = rms
+    rep["max_err"] = float(err.max()) if err.size else 0.0
+    rep["mean_err"] = float(err.mean()) if err.size else 0.0
+    rep["max_err_over_rms"] = rep["max_err"] / rms
+    assert rep["max_err"] <= OUT_TOL * rms, f"P4: max err {rep['max_err']:.4g} > {OUT_TOL} * RMS {rms:.4g}"
+    return rep

@@ -1,0 +1,193 @@
+"""GPU (sm_100a) parity of the C-ABI path against the CPU oracle (criteria P1-P8,
+SURVEY.md 8(c)); every call goes through libtarragon.so via the binding."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import workloads as wl
+from parity_util import compare, oracle_layer
+
+pytestmark = pytest.mark.gpu
+
+NT = min(32, os.cpu_count() or 1)
+
+
+def _tg():
+    import paper_2601_01310_b200 as tg
+    return tg
+
+
+def _setup(cfg, W, seed, T=None, skew=0.0, integer=False, shadows=True, T_max=None):
+    tg = _tg()
+    sh = wl.CONFIGS[cfg]
+    T = sh.T if T is None else T
+    u = None
+    if skew:
+        u = torch.randn(sh.d, generator=torch.Generator().manual_seed(seed + 99))
+        u = u / u.norm() * sh.d ** 0.5
+    L = wl.integer_layer(sh, seed) if integer else wl.make_layer(sh, seed, skew=skew, u=u)
+    x = wl.integer_tokens(sh, seed, T) if integer else wl.make_tokens(sh, seed, T, skew_mu=skew, u=u)
+    pl = wl.make_placement(sh.E, W, 1, shadows=shadows)
+    layer = tg.MoELayer(sh, pl, L, max_tokens_per_rank=T_max or max(T, 1))
+    return tg, sh, L, x, pl, layer
+
+
+def _run(layer, x):
+    xd = x.cuda()
+    out = layer(xd)
+    torch.cuda.synchronize()
+    return out
+
+
+def test_library_is_native_and_loaded():
+    tg = _tg()
+    import ctypes  # noqa: F401
+    assert os.path.exists(tg.LIB_PATH)
+    with open("/proc/self/maps") as f:
+        assert "libtarragon.so" in f.read()
+
+
+@pytest.mark.parametrize("skew", [0.0, 0.6])
+def test_tiny_parity_mask_poison_flip(skew):
+    """configs[0]: tiny layer, 2 logical EWs with shadows on one B200; EW1 masked mid-run."""
+    tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1000, skew=skew)
+    out0 = _run(layer, x)
+    rt = layer.routing(x.shape[0])
+    ref = oracle_layer(L, x, pl, [0, 0], G=1)
+    rep = compare(ref, wl.as_u16(out0), rt)
+    print("tiny", skew, rep)
+    # P6 determinism
+    out0b = _run(layer, x)
+    assert torch.equal(out0.view(torch.int16), out0b.view(torch.int16))
+    # P8 shadows idle when unmasked
+    st = layer.stats()
+    base = [tg.tg_bank_slot(layer.ctx, ew, 0) for ew in range(pl.n_ews)]
+    for ew in range(pl.n_ews):
+        for sl, e in enumerate(pl.hosted[ew]):
+            if e >= 0 and tuple(pl.cand[e, 0]) != (ew, sl):
+                assert st[0, base[ew] + sl] == 0
+    # P5 mask EW1 -> bit-identical; its slots poisoned with NaN
+    assert layer.mask_worker(1, 1) == tg.TG_OK
+    nan = torch.full((sh.F, sh.d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    nan2 = torch.full((sh.d, sh.F), float("nan"), dtype=torch.bfloat16, device="cuda")
+    for sl, e in enumerate(pl.hosted[1]):
+        if e >= 0:
+            tg.tg_load_experts(layer.ctx, 1, sl, e, nan, nan, nan2)
+    st0 = layer.stats()
+    out1 = _run(layer, x)
+    assert torch.equal(out0.view(torch.int16), out1.view(torch.int16)), "masked output differs"
+    st1 = layer.stats() - st0
+    for sl in range(pl.slots_per_ew):
+        assert st1[0, base[1] + sl] == 0, "masked EW received rows"
+    rt1 = layer.routing(x.shape[0])
+    ref1 = oracle_layer(L, x, pl, [0, 1], G=1)
+    compare(ref1, wl.as_u16(out1), rt1)
+
+
+def test_route_flip_bit_identity():
+    """configs[4] protocol on the tiny layer: table A (primaries first) / B (shadows first) alternate."""
+    tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1001)
+    outA = _run(layer, x)
+    for i in range(6):
+        cand = wl.flipped(pl.cand) if i % 2 == 0 else pl.cand
+        assert layer.set_route_table(cand) == tg.TG_OK
+        o = _run(layer, x)
+        assert torch.equal(outA.view(torch.int16), o.view(torch.int16)), f"flip {i} changed output"
+        rt = layer.routing(x.shape[0])
+        pl2 = wl.Placement(pl.n_ews, pl.ew_rank, pl.slots_per_ew, pl.hosted, cand)
+        ref = oracle_layer(L, x, pl2, [0, 0], G=1)
+        compare(ref, wl.as_u16(o), rt)
+    # stale versions are ignored
+    assert tg.tg_set_route_table(layer.ctx, layer.version, pl.cand) == tg.TG_ERR_STALE_VERSION
+
+
+def test_integer_ties_bit_exact():
+    """Integer router inputs: logits exact in any order, so lowest-id tie breaks must match exactly."""
+    tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1002, integer=True)
+    out = _run(layer, x)
+    rt = layer.routing(x.shape[0])
+    ref = oracle_layer(L, x, pl, [0, 0], G=1)
+    assert np.array_equal(rt["idx"].cpu().numpy(), ref["idx"])
+    assert (ref["gap"] == 0).sum() > 10, "test needs exact ties"
+    for kk in ("dst_rank", "dst_slot", "dst_pos"):
+        assert np.array_equal(rt[kk].cpu().numpy(), ref[kk])
+    ref["gap"][:] = 1.0  # no near-tie exemption
+    compare(ref, wl.as_u16(out), rt)
+
+
+@pytest.mark.parametrize("T", [1, 37, 300, 1000])
+def test_ragged_and_multi_tile(T):
+    """Ragged token counts; T = 1000 gives ~250 rows per expert -> 2 token tiles (128 + ragged)."""
+    tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1003 + T, T=T)
+    out = _run(layer, x)
+    rt = layer.routing(T)
+    ref = oracle_layer(L, x, pl, [0, 0], G=1)
+    compare(ref, wl.as_u16(out), rt)
+
+
+def test_empty_call_and_errors():
+    tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1004, T=16, T_max=64)
+    empty = torch.empty(0, sh.d, dtype=torch.bfloat16, device="cuda")
+    assert tg.tg_moe_layer(layer.ctx, empty, torch.empty_like(empty)) == tg.TG_OK
+    out = _run(layer, x)
+    ref = oracle_layer(L, x, pl, [0, 0], G=1)
+    compare(ref, wl.as_u16(out), layer.routing(16))
+    # too many tokens
+    big = torch.zeros(65, sh.d, dtype=torch.bfloat16, device="cuda")
+    assert tg.tg_moe_layer(layer.ctx, big, torch.empty_like(big)) == tg.TG_ERR_INVALID
+    # mask both EWs -> NO_ROUTE, nothing launched; unmask recovers
+    assert layer.mask_worker(0, 1) == tg.TG_OK
+    assert layer.mask_worker(1, 1) == tg.TG_ERR_NO_ROUTE
+    xd = x.cuda()
+    assert tg.tg_moe_layer(layer.ctx, xd, torch.empty_like(xd)) == tg.TG_ERR_NO_ROUTE
+    assert layer.mask_worker(0, 0) == tg.TG_OK
+    o2 = _run(layer, x)
+    assert torch.equal(out.view(torch.int16), o2.view(torch.int16))
+
+
+def test_host_entry_point_e2e():
+    """tg_moe_layer_host: pinned host in/out, copies inside the call."""
+    tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1005)
+    xh = x.pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    assert tg.tg_moe_layer_host(layer.ctx, xh, oh) == tg.TG_OK
+    torch.cuda.synchronize()
+    od = _run(layer, x)
+    assert torch.equal(oh.view(torch.int16), od.cpu().view(torch.int16))
+
+
+def _big(cfg, seed, n_sample, W=2, T=None):
+    tg, sh, L, x, pl, layer = _setup(cfg, W, seed=seed, T=T)
+    out = _run(layer, x)
+    rt = layer.routing(x.shape[0])
+    Tn = x.shape[0]
+    rng = np.random.default_rng(seed)
+    tok = np.sort(rng.choice(Tn, size=min(n_sample, Tn), replace=False)).astype(np.int32)
+    tok[0] = 0
+    tok[-1] = Tn - 1
+    ref = oracle_layer(L, x, pl, [0, 0], G=1, tokens=tok, n_threads=NT)
+    rep = compare(ref, wl.as_u16(out)[tok], rt, tokens=tok)
+    print(cfg, rep)
+    # mask EW1: bit-identical at full size
+    layer.mask_worker(1, 1)
+    out1 = _run(layer, x)
+    assert torch.equal(out.view(torch.int16), out1.view(torch.int16))
+    layer.close()
+    return rep
+
+
+def test_mixtral_decode_parity():
+    """configs[1]: Mixtral-shaped layer, T = 256 decode batch; routing for all tokens, FFN on a sample."""
+    _big("mixtral_decode", 2001, n_sample=24)
+
+
+def test_ds_v2_lite_shared_parity():
+    """configs[3] shape (64 experts top-6 + 2 shared merged to 2816) at T = 1024 on one GPU."""
+    _big("ds_v2_lite_decode", 2002, n_sample=48, W=8)
+
+
+def test_qwen_prefill_parity():
+    """configs[4] shape: 60 experts top-4, prefill T = 8192 (multi-tile slots)."""
+    _big("qwen_prefill", 2003, n_sample=48, W=4)
