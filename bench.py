@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the Tarragon MoE-layer round trip (tg_moe_layer) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
+
+N = 1 (default): BASELINE.json configs[1], Mixtral-8x7B-shaped layer (d 4096,
+8 experts top-2, F 14336), decode batch T = 256, bf16, one B200.
+N > 1 (torchrun, one rank per GPU): configs[2], the same layer with experts
+sharded as EWs over N GPUs (shadow replicas in residual HBM), T = 256 global
+tokens split over the ranks (strong scaling).
+A step = one tg_moe_layer call (router -> rank/exchange counts -> dispatch ->
+grouped SwiGLU expert GEMMs -> combine) over one synthetic batch.
+
+Prints ONE JSON line (rank 0).  `value` = tokens/s over the K timed steps
+(CUDA events on the launching stream, barrier + synchronize on both sides, max
+over ranks).  `e2e` = the same metric through tg_moe_layer_host (pinned host
+x in, out back to host, copies inside the timed region).  `roofline` = the
+GEMM kernel's algorithmic HBM bytes per launch / its mean event-timed
+duration inside the timed region, against MEASURED_PEAKS.json.
+`--impl reference` times the CPU oracle (the tier's reference arm) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as wl  # noqa: E402
+
+REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", 0)), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm," + ",".join("clocks_event_reasons." + r for r in REASONS)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, active = [], [], set()
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx.append(float(s[1]))
+            except Exception:
+                continue
+            for r, v in zip(REASONS, s[2:]):
+                if v.lower().startswith("active"):
+                    active.add(r)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(active),
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_weights_device(shape, seed, device, experts):
+    """Seeded synthetic weights of the configured architecture (random init), generated on the GPU."""
+    d, F = shape.d, shape.F
+    L = wl.Layer(shape, wl.bf16_normal((shape.E, d), d ** -0.5, seed * 1000 + 1, device), [None] * shape.E,
+                 [None] * shape.E, [None] * shape.E)
+    for e in experts:
+        L.w1[e] = wl.bf16_normal((F, d), d ** -0.5, seed * 1000 + 10 + 3 * e, device)
+        L.w3[e] = wl.bf16_normal((F, d), d ** -0.5, seed * 1000 + 11 + 3 * e, device)
+        L.w2[e] = wl.bf16_normal((d, F), F ** -0.5, seed * 1000 + 12 + 3 * e, device)
+    if shape.F_sh:
+        Fs = shape.F_sh
+        L.shared = (wl.bf16_normal((Fs, d), d ** -0.5, seed * 1000 + 2, device),
+                    wl.bf16_normal((Fs, d), d ** -0.5, seed * 1000 + 3, device),
+                    wl.bf16_normal((d, Fs), Fs ** -0.5, seed * 1000 + 4, device))
+    return L
+
+
+def gemm_algorithmic_bytes(shape, slot_rows_active, R_local):
+    """GEMM kernel (GK4) algorithmic HBM bytes per launch:
+    weights of every slot with rows (3*d*F*2 each) + shared weights + token rows
+    read (R*d*2) + expert outputs written (R*d*2)."""
+    b = slot_rows_active * 3 * shape.d * shape.F * 2 + 2 * R_local * shape.d * 2
+    if shape.F_sh:
+        b += 3 * shape.d * shape.F_sh * 2
+    return b
+
+
+def cpu_oracle_sample(shape, L_host, x_host, pl, n_tokens, n_threads):
+    """Time the oracle (as it stands) on the first n_tokens of the batch: O1..O8."""
+    import oracle
+    oracle.build()
+    w1 = [wl.as_u16(a) for a in L_host.w1]
+    w3 = [wl.as_u16(a) for a in L_host.w3]
+    w2 = [wl.as_u16(a) for a in L_host.w2]
+    sh = tuple(wl.as_u16(a) for a in L_host.shared) if L_host.shared is not None else None
+    xs = wl.as_u16(x_host[:n_tokens])
+    t0 = time.perf_counter()
+    r = oracle.layer(xs, wl.as_u16(L_host.wg), shape.k, w1, w3, w2, pl.cand, pl.ew_rank, pl.slots_per_ew,
+                     np.zeros(pl.n_ews, np.uint8), 1, shared=sh, n_threads=n_threads)
+    dt = time.perf_counter() - t0
+    assert r["rc"] == 0
+    return n_tokens / dt, dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, help="workloads.CONFIGS key (default mixtral_decode)")
+    ap.add_argument("--tokens", type=int, default=None, help="global tokens per call (default: config T)")
+    ap.add_argument("--cpu-sample", type=int, default=None, help="tokens in the oracle sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=1001)
+    args = ap.parse_args()
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    rank, world, local = dist_env()
+    N = world
+    cfg = args.config or "mixtral_decode"
+    shape = wl.CONFIGS[cfg]
+    T_glob = args.tokens or shape.T
+    assert T_glob % N == 0
+    T_r = T_glob // N
+    W = max(N, 1)
+    shadows = N > 1
+    pl = wl.make_placement(shape.E, W, N, shadows=shadows)
+    cores = os.cpu_count() or 1
+    config = {"workload": f"BASELINE configs[{1 if N == 1 else 2}]: {cfg} T={T_glob} global, "
+                          f"{W} EW(s){' + shadow replicas' if shadows else ''} on {N} B200",
+              "model": f"{cfg} (d={shape.d}, E={shape.E}, top-{shape.k}, F={shape.F}"
+                       f"{', F_sh=%d' % shape.F_sh if shape.F_sh else ''})",
+              "global_batch": T_glob, "seq_len": 1, "parallelism": f"ep{N}+dp{N}" if N > 1 else "single",
+              "l2": "weights (%.2f GB/GPU) >> 126 MB L2, streamed from HBM every step; 8 rotating x batches"
+                    % (3 * shape.d * shape.F * 2 * sum(1 for e in range(shape.E)
+                                                       if pl.ew_rank[pl.cand[e, 0, 0]] == 0) / 1e9)}
+
+    if args.impl == "reference":
+        # Reference arm of this tier: the CPU oracle, rank 0 only.
+        if rank != 0:
+            return
+        n = args.cpu_sample or 16
+        L = wl.make_layer(shape, args.seed)
+        x = wl.make_tokens(shape, args.seed, T=max(n, 1))
+        times = []
+        for _ in range(args.warmup if args.warmup < 3 else 1):
+            pass
+        for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
+            v, dt = cpu_oracle_sample(shape, L, x, pl, n, cores)
+            times.append(dt)
+        dt = float(np.median(times))
+        val = n / dt
+        line = {"impl": "reference", "metric": "MoE-layer tokens/s (oracle, CPU)", "value": val, "unit": "tokens/s",
+                "n_gpus": N, "steps": len(times), "warmup": 0, "ms_per_step": dt * 1e3,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                                 "sample": f"first {n} of the batch's tokens, full O1-O8 per step"},
+                "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import paper_2601_01310_b200 as tg
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if N > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    local_experts = sorted({e for ew in range(W) if pl.ew_rank[ew] == rank for e in pl.hosted[ew] if e >= 0})
+    L = make_weights_device(shape, args.seed, dev, local_experts)
+    layer = tg.MoELayer(shape, pl, L, max_tokens_per_rank=T_r, rank=rank, world=N, device=local, group=group)
+    NB = 8
+    xs = [wl.make_tokens(shape, args.seed + 17 * i, T=T_glob, device=dev)[rank * T_r:(rank + 1) * T_r].contiguous()
+          for i in range(NB)]
+    outs = [torch.empty_like(xs[0]) for _ in range(NB)]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if N > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def step(i):
+        rc = tg.tg_moe_layer(layer.ctx, xs[i % NB], outs[i % NB], stream)
+        if rc != tg.TG_OK:
+            raise tg.TarragonError(rc, tg.tg_last_error(layer.ctx))
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    tg.tg_set_profiling(layer.ctx, True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    ktimes = tg.tg_get_kernel_times(layer.ctx)
+    tg.tg_set_profiling(layer.ctx, False)
+    launches = tg.tg_last_launch_count(layer.ctx) * args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if N > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = T_glob * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public host-buffer entry point
+    xh = [x.cpu().pin_memory() for x in xs]
+    oh = [torch.empty_like(h).pin_memory() for h in xh]
+    for i in range(args.warmup):
+        tg.tg_moe_layer_host(layer.ctx, xh[i % NB], oh[i % NB], stream)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        rc = tg.tg_moe_layer_host(layer.ctx, xh[i % NB], oh[i % NB], stream)
+        assert rc == tg.TG_OK, tg.tg_last_error(layer.ctx)
+    e1.record(stream)
+    barrier()
+    ms_e = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    if N > 1:
+        torch.distributed.all_reduce(ms_e, op=torch.distributed.ReduceOp.MAX)
+    e2e_val = T_glob * args.steps / (float(ms_e.item()) / 1e3)
+
+    # ---- roofline of the dominant kernel (GEMM, GK4) on this rank
+    st = layer.routing(T_r)
+    counts = st["counts"].cpu().numpy()
+    rows_local = counts[rank]
+    active = int((rows_local > 0).sum())
+    R_local = int(rows_local.sum())
+    hbm, tf, tf_sus, src = peaks()
+    names = tg.KERNEL_NAMES
+    kt = dict(zip(names, ktimes))
+    g_ms = kt.get("gemm", float("nan"))
+    gbytes = gemm_algorithmic_bytes(shape, active, R_local)
+    achieved = gbytes / (g_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{cfg}:N{N}:T{T_glob}")
+    roof = {"bound": "hbm", "kernel": "k_gemm (GK4)", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
+            "algorithmic_bytes_per_launch": gbytes, "kernel_ms": g_ms,
+            "kernel_share_of_step": (g_ms / (ms / args.steps)) if ms else None,
+            "per_kernel_ms": kt}
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        n = args.cpu_sample or 16
+        Lh = wl.Layer(shape, L.wg.cpu(), [w.cpu() for w in L.w1], [w.cpu() for w in L.w3],
+                      [w.cpu() for w in L.w2], tuple(w.cpu() for w in L.shared) if L.shared else None)
+        v, dt = cpu_oracle_sample(shape, Lh, xs[0].cpu(), pl, n, cores)
+        cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {n} tokens of one batch through O1-O8 (fp64, {cores} threads over tokens), "
+                         f"{dt:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s", "n_gpus": N,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded random-init weights of the configured shape)", "config": config,
+                "clocks": clk.summary(), "gpu_launches": launches,
+                "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": T_glob * shape.d * 2,
+                        "d2h_bytes_per_step": T_glob * shape.d * 2},
+                "roofline": roof, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if N > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

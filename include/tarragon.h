@@ -152,9 +152,11 @@ int tg_bank_slot(const tg_ctx *ctx, int ew, int slot);
  * rank's tokens: int64 [world][S_max] host array.  Synchronises the device. */
 tg_status tg_get_stats(tg_ctx *ctx, int64_t *rows);
 
-/* Per-kernel CUDA-event timing of the following calls (on = 1).
- * tg_get_kernel_times(ctx, ms, &n): synchronises on the last call and writes
- * n (<= 8) durations in launch order: router, rank, dispatch, gemm, combine. */
+/* Per-kernel CUDA-event timing (events on the call's stream between launches,
+ * no host synchronisation per call).  tg_set_profiling(ctx, 1) starts a new
+ * record; tg_get_kernel_times(ctx, ms, &n) synchronises and writes n (= 5)
+ * MEAN durations in ms over the recorded calls (at most the last 512), in
+ * launch order: router, rank, dispatch, gemm, combine.                     */
 tg_status tg_set_profiling(tg_ctx *ctx, int on);
 tg_status tg_get_kernel_times(tg_ctx *ctx, float *ms, int *n);
 

@@ -80,9 +80,12 @@ struct tg_ctx {
   int last_launches = 0;
   bool sticky = false;
   // profiling
+  // profiling: 6 events per call, ring of kProfCalls calls, no host sync per call
+  static constexpr int kProfCalls = 512, kEv = 6;
   bool prof = false;
-  cudaEvent_t ev[8] = {nullptr};
-  int n_ev = 0;
+  std::vector<cudaEvent_t> ev;
+  int n_ev = 0;        // events recorded in the current call
+  int prof_calls = 0;  // calls recorded since tg_set_profiling(1)
   std::string errmsg = "no error";
 };
 
@@ -299,7 +302,6 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
     }
   }
   CKI(gemm_configure());
-  for (int i = 0; i < 8; ++i) CKI(cudaEventCreate(&c->ev[i]));
   CKI(cudaDeviceSynchronize());
 #undef CKI
   *out = c;
@@ -436,7 +438,9 @@ int tg_bank_slot(const tg_ctx *c, int ew, int slot) {
 }
 
 static void rec(tg_ctx *c, cudaStream_t s) {
-  if (c->prof && c->n_ev < 8) cudaEventRecord(c->ev[c->n_ev++], s);
+  if (!c->prof || c->ev.empty()) return;
+  int slot = c->prof_calls % tg_ctx::kProfCalls;
+  if (c->n_ev < tg_ctx::kEv) cudaEventRecord(c->ev[(size_t)slot * tg_ctx::kEv + c->n_ev++], s);
 }
 
 tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream) {
@@ -477,6 +481,7 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   rec(c, s);
   CK(launch_combine(a, s));
   rec(c, s);
+  if (c->prof) ++c->prof_calls;
   c->last_T = T;
   c->last_launches = (T > 0 ? 1 : 0) + 4;
   return TG_OK;
@@ -525,16 +530,39 @@ tg_status tg_get_stats(tg_ctx *c, int64_t *rows) {
 
 tg_status tg_set_profiling(tg_ctx *c, int on) {
   if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
   c->prof = on != 0;
+  c->prof_calls = 0;
+  if (c->prof && c->ev.empty()) {
+    CK(cudaSetDevice(c->device));
+    c->ev.resize((size_t)tg_ctx::kProfCalls * tg_ctx::kEv);
+    for (auto &e : c->ev) CK(cudaEventCreate(&e));
+  }
   return TG_OK;
 }
 
+// Mean per-kernel duration over the calls recorded since profiling was enabled
+// (at most the last kProfCalls): router, rank, dispatch, gemm, combine.
 tg_status tg_get_kernel_times(tg_ctx *c, float *ms, int *n) {
   if (!c || !ms || !n) return TG_ERR_INVALID;
-  if (!c->prof || c->n_ev < 2) { *n = 0; return TG_OK; }
-  CK(cudaEventSynchronize(c->ev[c->n_ev - 1]));
-  for (int i = 0; i + 1 < c->n_ev; ++i) CK(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
-  *n = c->n_ev - 1;
+  *n = 0;
+  if (!c->prof || c->prof_calls == 0) return TG_OK;
+  CK(cudaSetDevice(c->device));
+  const int calls = std::min(c->prof_calls, (int)tg_ctx::kProfCalls);
+  const int nk = tg_ctx::kEv - 1;
+  std::vector<double> acc(nk, 0.0);
+  for (int i = 0; i < calls; ++i) {
+    int slot = (c->prof_calls - 1 - i) % tg_ctx::kProfCalls;
+    cudaEvent_t *e = &c->ev[(size_t)slot * tg_ctx::kEv];
+    CK(cudaEventSynchronize(e[nk]));
+    for (int j = 0; j < nk; ++j) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, e[j], e[j + 1]));
+      acc[j] += t;
+    }
+  }
+  for (int j = 0; j < nk; ++j) ms[j] = (float)(acc[j] / calls);
+  *n = nk;
   return check_sticky(c);
 }
 
@@ -553,7 +581,7 @@ tg_status tg_finalize(tg_ctx *c) {
     cudaFree(c->w1s); cudaFree(c->w3s); cudaFree(c->w2s);
     cudaFree(c->sym); cudaFree(c->scratch);
     if (c->err_host) cudaFreeHost(c->err_host);
-    for (int i = 0; i < 8; ++i) if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    for (auto &e : c->ev) cudaEventDestroy(e);
   }
   delete c;
   return TG_OK;

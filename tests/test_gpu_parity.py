@@ -167,7 +167,7 @@ def _big(cfg, seed, n_sample, W=2, T=None):
     tok = np.sort(rng.choice(Tn, size=min(n_sample, Tn), replace=False)).astype(np.int32)
     tok[0] = 0
     tok[-1] = Tn - 1
-    ref = oracle_layer(L, x, pl, [0, 0], G=1, tokens=tok, n_threads=NT)
+    ref = oracle_layer(L, x, pl, [0] * W, G=1, tokens=tok, n_threads=NT)
     rep = compare(ref, wl.as_u16(out)[tok], rt, tokens=tok)
     print(cfg, rep)
     # mask EW1: bit-identical at full size
