@@ -154,11 +154,22 @@ tg_status tg_get_stats(tg_ctx *ctx, int64_t *rows);
 
 /* Per-kernel CUDA-event timing (events on the call's stream between launches,
  * no host synchronisation per call).  tg_set_profiling(ctx, 1) starts a new
- * record; tg_get_kernel_times(ctx, ms, &n) synchronises and writes n (= 5)
+ * record; tg_get_kernel_times(ctx, ms, &n) synchronises and writes n (= 2)
  * MEAN durations in ms over the recorded calls (at most the last 512), in
- * launch order: router, rank, dispatch, gemm, combine.                     */
+ * launch order: front (gate, rank, count exchange, dispatch) and gemm
+ * (grouped expert FFN + fused combine exchange + combine).                 */
 tg_status tg_set_profiling(tg_ctx *ctx, int on);
 tg_status tg_get_kernel_times(tg_ctx *ctx, float *ms, int *n);
+
+/* Diagnostics (performance analysis of the grouped GEMM kernel).
+ * tg_set_trace(ctx, 1): subsequent calls record, per GEMM work unit, its
+ * completion (globaltimer ns << 16 | unit kind << 12 | SM id), per CTA its
+ * start time, and phase timestamps of the front kernel.
+ * tg_get_trace(ctx, trace, cap, &n_units, &n_ctas) synchronises and copies
+ * the last call's records to the HOST array trace (uint64, cap entries):
+ * [0, n_units) unit records, then 148 CTA start stamps, then 64 phase stamps. */
+tg_status tg_set_trace(tg_ctx *ctx, int on);
+tg_status tg_get_trace(tg_ctx *ctx, uint64_t *trace, int cap, int *n_units, int *n_ctas);
 
 /* Kernel launches enqueued by the last tg_moe_layer call. */
 int tg_last_launch_count(const tg_ctx *ctx);

@@ -29,7 +29,7 @@ STATUS = {0: "TG_OK", -1: "TG_ERR_INVALID", -2: "TG_ERR_NO_ROUTE", -3: "TG_ERR_N
           -8: "TG_ERR_UNSUPPORTED"}
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2601_01310_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2601_01310_b200/build.py` "
                       "(there is no CPU fallback)")
 
 
@@ -61,6 +61,8 @@ _SIG = {
     "tg_set_profiling": ([_P, _I], _I),
     "tg_get_kernel_times": ([_P, _P, ctypes.POINTER(_I)], _I),
     "tg_last_launch_count": ([_P], _I),
+    "tg_set_trace": ([_P, _I], _I),
+    "tg_get_trace": ([_P, _P, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
     "tg_last_error": ([_P], ctypes.c_char_p),
     "tg_finalize": ([_P], _I),
 }
@@ -207,6 +209,26 @@ def tg_get_kernel_times(ctx):
     return [ms[i] for i in range(n.value)]
 
 
+def tg_set_trace(ctx, on=True):
+    _check(ctx, _lib.tg_set_trace(ctx, int(on)), "tg_set_trace")
+
+
+def tg_get_trace(ctx, cap=1 << 20):
+    """Last call's GEMM trace: dict(end ns[n_units], kind[n_units], smid[n_units], start ns[n_ctas],
+    front_stamps ns[16]) — end stamps keep the low 48 bits of globaltimer."""
+    tr = np.zeros(cap, np.uint64)
+    nu, nc = _I(0), _I(0)
+    _check(ctx, _lib.tg_get_trace(ctx, tr.ctypes.data, cap, ctypes.byref(nu), ctypes.byref(nc)), "tg_get_trace")
+    nu, nc = nu.value, nc.value
+    t = tr[:nu]
+    m48 = np.uint64((1 << 48) - 1)
+    return dict(end=(t >> np.uint64(16)).astype(np.int64),
+                kind=((t >> np.uint64(12)) & np.uint64(0xF)).astype(np.int64),
+                smid=(t & np.uint64(0xFFF)).astype(np.int64),
+                start=(tr[nu:nu + nc] & m48).astype(np.int64),
+                front_stamps=(tr[nu + 148:nu + 148 + 16] & m48).astype(np.int64))
+
+
 def tg_last_launch_count(ctx) -> int:
     return _lib.tg_last_launch_count(ctx)
 
@@ -216,7 +238,7 @@ def tg_finalize(ctx):
         _lib.tg_finalize(ctx)
 
 
-KERNEL_NAMES = ("router", "rank", "dispatch", "gemm", "combine")
+KERNEL_NAMES = ("front", "gemm")
 
 
 # ----------------------------------------------------------------- convenience

@@ -1,6 +1,6 @@
 """Build libtarragon.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-    python -m paper_2601_01310_b200.build [--force] [--verbose]
+    python paper_2601_01310_b200/build.py [--force] [--verbose]
 
 The shared library links the CUDA runtime statically and resolves the driver
 entry point it needs (cuTensorMapEncodeTiled) at run time, so it loads (and

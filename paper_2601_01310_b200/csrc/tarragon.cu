@@ -74,6 +74,8 @@ struct tg_ctx {
   CallArgs args{};
   TmaMaps maps{};
   int *err_host = nullptr, *err_dev = nullptr;
+  uint64_t *trace = nullptr;                     // device trace buffer (diagnostics)
+  bool tracing = false;
   bf16 *x_stage = nullptr, *out_stage = nullptr;   // for tg_moe_layer_host
   uint32_t epoch = 0;
   int last_T = 0;
@@ -81,7 +83,7 @@ struct tg_ctx {
   bool sticky = false;
   // profiling
   // profiling: 6 events per call, ring of kProfCalls calls, no host sync per call
-  static constexpr int kProfCalls = 512, kEv = 6;
+  static constexpr int kProfCalls = 512, kEv = 3;
   bool prof = false;
   std::vector<cudaEvent_t> ev;
   int n_ev = 0;        // events recorded in the current call
@@ -179,6 +181,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   for (int r = 0; r < world; ++r) c->S_max = std::max(c->S_max, c->S_of_rank[r]);
   c->S_loc = c->S_of_rank[rank];
   c->nkeys = world * c->S_max;
+  if (c->S_loc > kMaxSlotsPerRank) { delete c; return fail(nullptr, TG_ERR_INVALID, "%d slots on rank %d > %d", c->S_loc, rank, kMaxSlotsPerRank); }
   if (c->nkeys > kMaxKeys) { delete c; return fail(nullptr, TG_ERR_INVALID, "world * slots per rank = %d > %d", c->nkeys, kMaxKeys); }
   c->hosted.assign((size_t)c->W * c->spe, -1);
   c->mask.assign(c->W, 0);
@@ -189,7 +192,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   c->R_sh0 = c->R_cap;
   c->R_tot = c->R_cap + (Fsh > 0 ? c->T_max : 0);
   // fixed split-K for long GEMM2 reductions: a function of the shape only
-  c->nsplit = (F / BK >= 128 && (F / BK) % 2 == 0) ? 2 : 1;
+  c->nsplit = (F / BK >= 128 && (F / BK) % 4 == 0) ? 4 : (F / BK >= 128 && (F / BK) % 2 == 0) ? 2 : 1;
   if (cuda_device < 0) { *out = c; return TG_OK; }
 
   // ---------------------------------------------------------------- device
@@ -250,7 +253,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
   size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
   size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(64);
-  size_t o_ctr = carve((size_t)c->args.n_ctr_max * 4), o_units = carve((size_t)c->args.n_units_max * sizeof(Unit));
+  size_t o_ctr = carve((size_t)c->args.n_ctr_max * 4);
   size_t o_nu = carve(16);
   size_t o_H = carve((size_t)c->R_cap * F * 2);
   size_t o_Hs = carve(Fsh > 0 ? Tm * Fsh * 2 : 0);
@@ -269,7 +272,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   a.lrank = (int32_t *)(sb + o_lrank); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
   a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
   a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
-  a.sync = (int32_t *)(sb + o_sync); a.ctr = (int32_t *)(sb + o_ctr); a.units = (Unit *)(sb + o_units);
+  a.sync = (int32_t *)(sb + o_sync); a.ctr = (int32_t *)(sb + o_ctr);
   a.n_units = (int32_t *)(sb + o_nu);
   a.H = (bf16 *)(sb + o_H); a.Hs = Fsh > 0 ? (bf16 *)(sb + o_Hs) : nullptr;
   a.ws = c->nsplit > 1 ? (float *)(sb + o_ws) : nullptr; a.ysh = Fsh > 0 ? (bf16 *)(sb + o_ysh) : nullptr;
@@ -468,22 +471,17 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   a.x = reinterpret_cast<const bf16 *>(x);
   a.out = reinterpret_cast<bf16 *>(out);
   a.epoch = ++c->epoch;
+  a.trace = c->tracing ? c->trace : nullptr;
   for (int q = 0; q < kMaxWorld; ++q) a.sym[q] = q < c->world ? c->peer[q] : nullptr;
   c->n_ev = 0;
   rec(c, s);
-  CK(launch_router(a, rk, s));
-  rec(c, s);
-  CK(launch_rank(a, s));
-  rec(c, s);
-  CK(launch_dispatch(a, s));
+  CK(launch_front(a, rk, c->n_sms, s));
   rec(c, s);
   CK(launch_gemm(a, c->maps, c->n_sms, s));
   rec(c, s);
-  CK(launch_combine(a, s));
-  rec(c, s);
   if (c->prof) ++c->prof_calls;
   c->last_T = T;
-  c->last_launches = (T > 0 ? 1 : 0) + 4;
+  c->last_launches = 2;
   return TG_OK;
 }
 
@@ -566,6 +564,35 @@ tg_status tg_get_kernel_times(tg_ctx *c, float *ms, int *n) {
   return check_sticky(c);
 }
 
+tg_status tg_set_trace(tg_ctx *c, int on) {
+  if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
+  CK(cudaSetDevice(c->device));
+  if (on && !c->trace) {
+    CK(cudaMalloc(&c->trace, sizeof(uint64_t) * ((size_t)c->args.n_units_max + 148 + 64)));
+    CK(cudaMemset(c->trace, 0, sizeof(uint64_t) * ((size_t)c->args.n_units_max + 148 + 64)));
+  }
+  c->tracing = on != 0;
+  return TG_OK;
+}
+
+tg_status tg_get_trace(tg_ctx *c, uint64_t *trace, int cap, int *n_units, int *n_ctas) {
+  if (!c || !n_units || !n_ctas) return TG_ERR_INVALID;
+  if (c->host_only || !c->trace) return fail(c, TG_ERR_UNSUPPORTED, "tracing not enabled");
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());
+  int nu = 0;
+  CK(cudaMemcpy(&nu, c->args.n_units, sizeof(int), cudaMemcpyDeviceToHost));
+  *n_units = nu;
+  *n_ctas = c->n_sms;
+  if (nu + 148 + 64 > cap) return fail(c, TG_ERR_INVALID, "trace capacity %d < %d", cap, nu + 148 + 64);
+  if (trace) {
+    CK(cudaMemcpy(trace, c->trace, sizeof(uint64_t) * nu, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(trace + nu, c->trace + c->args.n_units_max, sizeof(uint64_t) * (148 + 64), cudaMemcpyDeviceToHost));
+  }
+  return check_sticky(c);
+}
+
 int tg_last_launch_count(const tg_ctx *c) { return c ? c->last_launches : 0; }
 
 const char *tg_last_error(const tg_ctx *c) { return c ? c->errmsg.c_str() : g_init_error.c_str(); }
@@ -579,7 +606,7 @@ tg_status tg_finalize(tg_ctx *c) {
       if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer[q]);
     cudaFree(c->bank_w1); cudaFree(c->bank_w3); cudaFree(c->bank_w2); cudaFree(c->wg);
     cudaFree(c->w1s); cudaFree(c->w3s); cudaFree(c->w2s);
-    cudaFree(c->sym); cudaFree(c->scratch);
+    cudaFree(c->sym); cudaFree(c->scratch); cudaFree(c->trace);
     if (c->err_host) cudaFreeHost(c->err_host);
     for (auto &e : c->ev) cudaEventDestroy(e);
   }

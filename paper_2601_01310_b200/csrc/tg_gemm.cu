@@ -1,28 +1,35 @@
-// tg_gemm.cu — GK4: persistent grouped expert-FFN kernel for sm_100a.
+// tg_gemm.cu — GK4+GK5: persistent grouped expert-FFN kernel for sm_100a, with
+// the combine exchange fused into the GEMM2 epilogue and the weighted
+// unpermute (combine) run by the same CTAs after a grid barrier.
 //
 // One launch runs every expert FFN this rank serves as EW (§2.2.1: "an
 // EW aggregates requests for the same layer and expert, and executes them as
-// a single large batch"), in two dependent phases over a device-built work
-// list (GK2):
-//   GEMM1 units:  [a1 | a3] = W1|W3 (128 x d tile)  .  X^T (d x n tokens)
-//                 h = bf16(silu(a1) * a3)  -> H          (SwiGLU, R#6/R#7)
+// a single large batch") over a work list decoded on the fly from the per-slot
+// row counts of this call:
+//   GEMM1 units:  [a1 | a3] = W1|W3 (128 x d tile) . X^T (d x n tokens),
+//                 h = bf16(silu(a1) * a3) -> H                 (SwiGLU, R#6/R#7)
 //   GEMM2 units:  y = W2 (128 x F tile) . H^T, fixed split-K for long F with an
 //                 in-order reduction; y = bf16(.) stored straight into the
 //                 source AW's combine buffer slot [t][j] (NVLink store when the
-//                 source is a peer): the combine exchange fused in the epilogue.
-// Swap-AB: the weight tile fills UMMA M = 128, the (few) tokens of a slot are
-// UMMA N (16..128), so decode batches waste no tensor-core rows.
+//                 source is a peer): the combine exchange, fused.
+//   combine:      out[t] = bf16(sum_j w[t,j] y[t,j] (+ y_sh[t])), fp32, j order
+//                 (§2.1 "aggregated via a weighted sum").
+// Swap-AB: the weight tile fills UMMA M = 128 and the tokens of a slot are UMMA
+// N (16..128), so decode batches waste no tensor-core rows.
 //
 // Warp roles (256 threads, 1 CTA / SM, persistent over an atomic work queue):
 //   w0  TMA producer: fetches unit ids, streams W and X/H tiles (128-B swizzle)
-//       into a 4-stage smem ring (mbarrier full/empty, complete_tx bytes).
+//       into a 4-stage smem ring (mbarrier full/empty, complete_tx bytes);
+//       one stage carries 1-2 K blocks so every stage holds >= 32 KB of weights.
 //   w1  MMA issuer: one thread issues tcgen05.mma (bf16 -> fp32 in TMEM), two
 //       TMEM accumulator buffers so the epilogue overlaps the next unit.
-//   w2  TMEM allocator.      w4-7  epilogue: tcgen05.ld -> regs -> global.
+//   w2  TMEM allocator.   w3  slot plan.   w4-7  epilogue: tcgen05.ld -> global.
 #include "tg_internal.h"
 #include "tg_ptx.cuh"
 
 namespace tg {
+
+constexpr int kMaxPlan = kMaxSlotsPerRank + 2;
 
 struct GemmShared {
   uint64_t full[kStages];
@@ -34,11 +41,143 @@ struct GemmShared {
   int sched[kSchedDepth];
   uint32_t tmem_base;
   int red_last;
+  // slot plan of this call (routed slots, then the shared pseudo-slot)
+  int NS, G1, total, ngroups;
+  int nt[kMaxPlan];        // token tiles per slot
+  int rows[kMaxPlan];      // rows per slot
+  int rowoff[kMaxPlan];    // first recv row
+  int g1off[kMaxPlan];     // GEMM1 unit offsets
+  int g2off[kMaxPlan];     // GEMM2 unit offsets
+  int goff[kMaxPlan];      // dependency-group offsets
+  int roff[kMaxPlan];      // reduction-group offsets
 };
 
 __device__ __forceinline__ float silu_f(float a) { return __fdiv_rn(a, 1.0f + expf(-a)); }
 
 __device__ __forceinline__ int box_index(int nrows) { return ((nrows + 15) >> 4) - 1; }
+
+// Warp-parallel exclusive scan of per-slot quantities (lanes own contiguous slot ranges).
+__device__ void build_plan(const CallArgs &a, GemmShared *P) {
+  const int lane = threadIdx.x & 31;
+  const int S = a.S_loc, nsh = a.Fsh > 0 ? 1 : 0, NS = S + nsh;
+  const int ftiles = (a.F + BM - 1) / BM, ctiles = (a.d + BM - 1) / BM;
+  const int ftiles_sh = nsh ? (a.Fsh + BM - 1) / BM : 0;
+  const int per = (NS + 31) / 32;
+  const int s0 = min(NS, lane * per), s1 = min(NS, s0 + per);
+  int sr = 0, su1 = 0, su2 = 0, sg = 0, sred = 0;
+  for (int s = s0; s < s1; ++s) {
+    const bool sh = (s == S);
+    const int rows = sh ? a.T : __ldcg(a.slot_rows + s);
+    const int nt = (rows + BN_MAX - 1) / BN_MAX;
+    const int ns = sh ? 1 : a.nsplit;
+    P->rows[s] = rows;
+    P->nt[s] = nt;
+    sr += sh ? 0 : rows;
+    su1 += nt * (sh ? ftiles_sh : ftiles);
+    su2 += nt * ctiles * ns;
+    sg += nt;
+    sred += (ns > 1) ? nt * ctiles : 0;
+  }
+  auto xscan = [&](int v) {
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int n = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += n;
+    }
+    return incl - v;
+  };
+  int br = xscan(sr), bu1 = xscan(su1), bu2 = xscan(su2), bg = xscan(sg), bred = xscan(sred);
+  for (int s = s0; s < s1; ++s) {
+    const bool sh = (s == S);
+    const int nt = P->nt[s];
+    const int ns = sh ? 1 : a.nsplit;
+    P->rowoff[s] = sh ? a.R_sh0 : br;
+    P->g1off[s] = bu1;
+    P->g2off[s] = bu2;
+    P->goff[s] = bg;
+    P->roff[s] = bred;
+    br += sh ? 0 : P->rows[s];
+    bu1 += nt * (sh ? ftiles_sh : ftiles);
+    bu2 += nt * ctiles * ns;
+    bg += nt;
+    bred += (ns > 1) ? nt * ctiles : 0;
+  }
+  if (lane == 31) {
+    P->g1off[NS] = bu1;
+    P->g2off[NS] = bu2;
+    P->goff[NS] = bg;
+    P->roff[NS] = bred;
+    P->NS = NS;
+    P->G1 = bu1;
+    P->total = bu1 + bu2;
+    P->ngroups = bg;
+    if (blockIdx.x == 0) *a.n_units = bu1 + bu2;
+    if (bg + bred > a.n_ctr_max) {  // capacity guard (sized at init for the worst case)
+      atomicExch(a.err, 0x4003);
+      P->total = 0;
+    }
+  }
+}
+
+__device__ __forceinline__ int find_seg(const int *off, int n, int u) {
+  int lo = 0, hi = n;  // off[lo] <= u < off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= u) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Unit u of this call's work list: GEMM1 (slot, f-tile, n-tile), then GEMM2
+// (slot, c-tile, n-tile, split).  Counters: per (slot, n-tile) for the GEMM1 ->
+// GEMM2 dependency; per (slot, c-tile, n-tile) for the split-K reduction.
+__device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared *P, int u) {
+  Unit U;
+  const int S = a.S_loc, NS = P->NS;
+  const int ftiles = (a.F + BM - 1) / BM;
+  if (u < P->G1) {
+    const int s = find_seg(P->g1off, NS, u);
+    const bool sh = (s == S);
+    const int loc = u - P->g1off[s];
+    const int f = loc / P->nt[s], n = loc % P->nt[s];
+    U.kind = sh ? U_G1_SH : U_G1;
+    U.slot = sh ? 0 : s;
+    U.m0 = f * BM;
+    U.n0 = P->rowoff[s] + n * BN_MAX;
+    U.nrows = min(BN_MAX, P->rows[s] - n * BN_MAX);
+    U.kb0 = 0;
+    U.kb1 = a.d / BK;
+    U.dep = P->goff[s] + n;
+    U.red = -1;
+    U.split = 0;
+    U.nsplit = 1;
+    U.dep_target = 0;
+  } else {
+    const int u2 = u - P->G1;
+    const int s = find_seg(P->g2off, NS, u2);
+    const bool sh = (s == S);
+    const int ns = sh ? 1 : a.nsplit;
+    const int nt = P->nt[s];
+    const int loc = u2 - P->g2off[s];
+    const int c = loc / (nt * ns), rem = loc % (nt * ns);
+    const int n = rem / ns, sp = rem % ns;
+    const int kbF = (sh ? a.Fsh : a.F) / BK;
+    U.kind = sh ? U_G2_SH : U_G2;
+    U.slot = sh ? 0 : s;
+    U.m0 = c * BM;
+    U.n0 = P->rowoff[s] + n * BN_MAX;
+    U.nrows = min(BN_MAX, P->rows[s] - n * BN_MAX);
+    U.kb0 = sp * (kbF / ns);
+    U.kb1 = (sp + 1) * (kbF / ns);
+    U.dep = P->goff[s] + n;
+    U.dep_target = sh ? (a.Fsh + BM - 1) / BM : ftiles;
+    U.red = (ns > 1) ? P->goff[NS] + P->roff[s] + c * nt + n : -1;
+    U.split = sp;
+    U.nsplit = ns;
+  }
+  return U;
+}
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ TmaMaps maps, const __grid_constant__ CallArgs a) {
@@ -50,12 +189,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int *err = a.err;
+  const bool sys = a.world > 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) { mbar_init(&S->full[i], 1); mbar_init(&S->empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&S->tfull[i], 1); mbar_init(&S->tempty[i], 128); }
     for (int i = 0; i < kSchedDepth; ++i) { mbar_init(&S->sfull[i], 1); mbar_init(&S->sempty[i], 5); }
     fence_barrier_init();
+    if (a.trace) a.trace[a.n_units_max + blockIdx.x] = globaltimer_ns();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.w1);
@@ -66,11 +207,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tmem_alloc(&S->tmem_base, kTmemCols);
     tmem_relinquish();
   }
+  if (warp == 3) build_plan(a, S);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S->tmem_base;
-  const int n_units = *reinterpret_cast<volatile int *>(a.n_units);
+  const int n_units = S->total;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -80,10 +222,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // Dispatched rows from peers must have landed (release/acquire on
       // per-source epoch flags), then order them before async-proxy reads.
       for (int src = 0; src < a.world; ++src) {
-        if (a.need_src[src]) {
+        if (__ldcg(a.need_src + src)) {
           const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
                                FLAG_DATA * kMaxWorld + src;
-          wait_flag_ge(fl, a.epoch, err, 0x4001);
+          wait_flag_ge_s(fl, a.epoch, sys, err, 0x4001);
         }
       }
       fence_proxy_async_global();
@@ -97,7 +239,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         S->sched[r] = u;
         mbar_arrive(&S->sfull[r]);
         if (u < 0) break;
-        const Unit U = a.units[u];
+        const Unit U = decode_unit(a, S, u);
         const bool g1 = (U.kind == U_G1 || U.kind == U_G1_SH);
         const bool sh = (U.kind == U_G1_SH || U.kind == U_G2_SH);
         if (!g1) {
@@ -107,18 +249,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         const int bi = box_index(U.nrows);
         const uint32_t bbytes = (uint32_t)(bi + 1) * 16 * BK * 2;
+        const uint32_t abytes = (g1 ? 2u : 1u) * kTileBytes;
+        const uint32_t sub = abytes + bbytes;             // one 64-wide K block of A tile(s) + B tile
+        const int kps = max(1, (int)(kStageBytes / sub));  // K blocks per stage (2 for decode GEMM2)
         const CUtensorMap *mA0 = g1 ? (sh ? &maps.w1s : &maps.w1) : (sh ? &maps.w2s : &maps.w2);
         const CUtensorMap *mA1 = sh ? &maps.w3s : &maps.w3;
         const CUtensorMap *mB = g1 ? &maps.x[bi] : (sh ? &maps.hs[bi] : &maps.h[bi]);
         const int rowA = g1 ? U.slot * (sh ? a.Fsh : a.F) + U.m0 : U.slot * a.d + U.m0;
         const int rowB = (!g1 && sh) ? U.n0 - a.R_sh0 : U.n0;
-        for (int kb = U.kb0; kb < U.kb1; ++kb) {
+        for (int kb = U.kb0; kb < U.kb1; kb += kps) {
+          const int cnt = min(kps, U.kb1 - kb);
           mbar_wait(&S->empty[stage], phase ^ 1, err);
           uint8_t *st = ring + stage * kStageBytes;
-          mbar_arrive_expect_tx(&S->full[stage], (g1 ? 2u : 1u) * kTileBytes + bbytes);
-          tma_load_2d(st, mA0, &S->full[stage], kb * BK, rowA, pol_w);
-          if (g1) tma_load_2d(st + kTileBytes, mA1, &S->full[stage], kb * BK, rowA, pol_w);
-          tma_load_2d(st + 2 * kTileBytes, mB, &S->full[stage], kb * BK, rowB, pol_x);
+          mbar_arrive_expect_tx(&S->full[stage], (uint32_t)cnt * sub);
+          for (int i = 0; i < cnt; ++i) {
+            uint8_t *sb = st + i * sub;
+            tma_load_2d(sb, mA0, &S->full[stage], (kb + i) * BK, rowA, pol_w);
+            if (g1) tma_load_2d(sb + kTileBytes, mA1, &S->full[stage], (kb + i) * BK, rowA, pol_w);
+            tma_load_2d(sb + abytes, mB, &S->full[stage], (kb + i) * BK, rowB, pol_x);
+          }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -134,7 +283,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int u = S->sched[r];
         mbar_arrive(&S->sempty[r]);
         if (u < 0) break;
-        const Unit U = a.units[u];
+        const Unit U = decode_unit(a, S, u);
         const bool g1 = (U.kind == U_G1 || U.kind == U_G1_SH);
         const int buf = it & 1;
         mbar_wait(&S->tempty[buf], ((it >> 1) & 1) ^ 1, err);
@@ -142,19 +291,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int nb = (box_index(U.nrows) + 1) * 16;
         const uint32_t idesc = idesc_bf16_f32(BM, nb);
         const uint32_t d0 = tmem + buf * 256, d1 = tmem + buf * 256 + 128;
-        for (int kb = U.kb0; kb < U.kb1; ++kb) {
+        const uint32_t abytes = (g1 ? 2u : 1u) * kTileBytes;
+        const uint32_t sub = abytes + (uint32_t)nb * BK * 2;
+        const int kps = max(1, (int)(kStageBytes / sub));
+        for (int kb = U.kb0; kb < U.kb1; kb += kps) {
+          const int cnt = min(kps, U.kb1 - kb);
           mbar_wait(&S->full[stage], phase, err);
           tc_fence_after();
-          const uint32_t sa = smem_u32(ring + stage * kStageBytes);
-          const uint64_t dA0 = desc_sw128_kmajor(sa);
-          const uint64_t dA1 = desc_sw128_kmajor(sa + kTileBytes);
-          const uint64_t dB = desc_sw128_kmajor(sa + 2 * kTileBytes);
+          for (int i = 0; i < cnt; ++i) {
+            const uint32_t sa = smem_u32(ring + stage * kStageBytes + i * sub);
+            const uint64_t dA0 = desc_sw128_kmajor(sa);
+            const uint64_t dA1 = desc_sw128_kmajor(sa + kTileBytes);
+            const uint64_t dB = desc_sw128_kmajor(sa + abytes);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t acc = (kb > U.kb0 || kk > 0) ? 1u : 0u;
-            // advance 16 K-elements = 32 B inside the swizzle row (>>4 units)
-            umma_bf16_ss(d0, dA0 + 2 * kk, dB + 2 * kk, idesc, acc);
-            if (g1) umma_bf16_ss(d1, dA1 + 2 * kk, dB + 2 * kk, idesc, acc);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t acc = (kb > U.kb0 || i > 0 || kk > 0) ? 1u : 0u;
+              // advance 16 K-elements = 32 B inside the swizzle row (>>4 units)
+              umma_bf16_ss(d0, dA0 + 2 * kk, dB + 2 * kk, idesc, acc);
+              if (g1) umma_bf16_ss(d1, dA1 + 2 * kk, dB + 2 * kk, idesc, acc);
+            }
           }
           umma_commit(&S->empty[stage]);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -166,6 +321,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ===================== epilogue (128 threads) =====================
     const int q = warp & 3;            // TMEM lane quarter of this warp
     const int et = threadIdx.x - 128;  // 0..127
+    const int2 *meta = reinterpret_cast<const int2 *>(a.sym[a.rank] + a.L.meta);
     for (int it = 0;; ++it) {
       const int r = it % kSchedDepth;
       mbar_wait(&S->sfull[r], (it / kSchedDepth) & 1, err);
@@ -173,7 +329,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&S->sempty[r]);
       if (u < 0) break;
-      const Unit U = a.units[u];
+      const Unit U = decode_unit(a, S, u);
       const bool g1 = (U.kind == U_G1 || U.kind == U_G1_SH);
       const bool sh = (U.kind == U_G1_SH || U.kind == U_G2_SH);
       const int buf = it & 1;
@@ -212,7 +368,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       } else {
         const bool split = (U.nsplit > 1);
-        const int2 *meta = reinterpret_cast<const int2 *>(a.sym[a.rank] + a.L.meta);
         for (int c0 = 0; c0 < U.nrows; c0 += 32) {
           uint32_t r1[32];
           tmem_ld_32x32b_x32(tbase + c0, r1);
@@ -239,41 +394,71 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         mbar_arrive(&S->tempty[buf]);
         if (split) {
-          // fixed-order split-K reduction by the last split to finish
+          // fixed-order split-K reduction ((p0 + p1) + p2) + ... by the last split to finish
           __threadfence();
           named_bar_sync(1, 128);
           if (et == 0) S->red_last = (atomicAdd(a.ctr + U.red, 1) == U.nsplit - 1);
           named_bar_sync(1, 128);
           if (S->red_last) {
             __threadfence();
-            if (m < a.d) {
-              for (int n = 0; n < U.nrows; ++n) {
-                const int row = U.n0 + n;
-                float acc = __ldcg(a.ws + (size_t)row * a.d + m);
-                for (int sp = 1; sp < U.nsplit; ++sp)
-                  acc = __fadd_rn(acc, __ldcg(a.ws + ((size_t)sp * a.R_cap + row) * a.d + m));
-                const int2 o = meta[row];
-                bf16 *yb = reinterpret_cast<bf16 *>(a.sym[o.x] + a.L.ybuf);
-                yb[(size_t)o.y * a.d + m] = __float2bfloat16_rn(acc);
+            // 128 threads: 4 row groups x 32 threads x 4 consecutive columns (16-B loads);
+            // y[row][c] = bf16(((p0 + p1) + p2) + ...), 8-B bf16 stores to the source AW.
+            const int cg = (et & 31) * 4, rg = et >> 5;
+            const int c = U.m0 + cg;
+            if (c < a.d) {
+              for (int n0 = rg; n0 < U.nrows; n0 += 16) {
+                float4 acc[4];
+                int2 o[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const int n = n0 + 4 * i;
+                  const bool v = n < U.nrows;
+                  acc[i] = v ? __ldcg(reinterpret_cast<const float4 *>(a.ws + (size_t)(U.n0 + n) * a.d + c))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                  o[i] = v ? meta[U.n0 + n] : make_int2(0, 0);
+                }
+                for (int sp = 1; sp < U.nsplit; ++sp) {
+                  float4 p[4];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    const int n = n0 + 4 * i;
+                    p[i] = (n < U.nrows) ? __ldcg(reinterpret_cast<const float4 *>(
+                                               a.ws + ((size_t)sp * a.R_cap + U.n0 + n) * a.d + c))
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                  }
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    acc[i].x = __fadd_rn(acc[i].x, p[i].x);
+                    acc[i].y = __fadd_rn(acc[i].y, p[i].y);
+                    acc[i].z = __fadd_rn(acc[i].z, p[i].z);
+                    acc[i].w = __fadd_rn(acc[i].w, p[i].w);
+                  }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  if (n0 + 4 * i < U.nrows) {
+                    __nv_bfloat162 lo = __floats2bfloat162_rn(acc[i].x, acc[i].y);
+                    __nv_bfloat162 hi = __floats2bfloat162_rn(acc[i].z, acc[i].w);
+                    uint2 pk;
+                    pk.x = *reinterpret_cast<uint32_t *>(&lo);
+                    pk.y = *reinterpret_cast<uint32_t *>(&hi);
+                    bf16 *yb = reinterpret_cast<bf16 *>(a.sym[o[i].x] + a.L.ybuf);
+                    *reinterpret_cast<uint2 *>(yb + (size_t)o[i].y * a.d + c) = pk;
+                  }
+                }
               }
             }
           }
           named_bar_sync(1, 128);
         }
       }
-    }
-    // all units of this CTA done: the last CTA releases the combine flags
-    __threadfence_system();
-    named_bar_sync(1, 128);
-    if (et == 0) {
-      if (atomicAdd(&a.sync[2], 1) == (int)gridDim.x - 1) {
-        __threadfence_system();
-        for (int src = 0; src < a.world; ++src) {
-          uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[src] + a.L.flags) + FLAG_COMB * kMaxWorld + a.rank;
-          st_release_sys(fl, a.epoch);
-        }
+      if (a.trace && et == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[u] = (globaltimer_ns() << 16) | ((uint64_t)U.kind << 12) | (smid & 0xFFF);
       }
     }
+    fence_scope(sys);  // this CTA's y rows (possibly on peers) before the grid barrier
   }
   tc_fence_before();
   __syncthreads();
@@ -281,6 +466,59 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
   }
+
+  // ===================== combine (GK5), all CTAs =====================
+  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 10);
+  grid_barrier(gbar, a.epoch, 1, 0, err);
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 8] = globaltimer_ns();
+  if (blockIdx.x == 0 && threadIdx.x < a.world) {
+    // every expert output this rank computed is in its source's combine buffer
+    fence_scope(sys);
+    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[threadIdx.x] + a.L.flags) + FLAG_COMB * kMaxWorld + a.rank;
+    st_release(fl, a.epoch, sys);
+  }
+  if (threadIdx.x < a.world && __ldcg(a.sent_to + threadIdx.x)) {
+    const uint32_t *fl =
+        reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + FLAG_COMB * kMaxWorld + threadIdx.x;
+    wait_flag_ge_s(fl, a.epoch, sys, err, 0x5001);
+  }
+  __syncthreads();
+  const int nch = a.d >> 3;
+  const size_t total = (size_t)a.T * nch;
+  const bf16 *ybuf = reinterpret_cast<const bf16 *>(a.sym[a.rank] + a.L.ybuf);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / nch), c8 = (int)(i % nch);
+    float acc[8];
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) acc[qq] = 0.f;
+    for (int j = 0; j < a.k; ++j) {
+      const float wj = __ldcg(a.w + (size_t)t * a.k + j);
+      uint4 v = __ldcg(reinterpret_cast<const uint4 *>(ybuf + ((size_t)t * a.k + j) * a.d) + c8);
+      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        float2 f = __bfloat1622float2(vp[qq]);
+        acc[2 * qq] = __fmaf_rn(wj, f.x, acc[2 * qq]);
+        acc[2 * qq + 1] = __fmaf_rn(wj, f.y, acc[2 * qq + 1]);
+      }
+    }
+    if (a.Fsh > 0) {
+      uint4 v = __ldcg(reinterpret_cast<const uint4 *>(a.ysh + (size_t)t * a.d) + c8);
+      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        float2 f = __bfloat1622float2(vp[qq]);
+        acc[2 * qq] = __fadd_rn(acc[2 * qq], f.x);
+        acc[2 * qq + 1] = __fadd_rn(acc[2 * qq + 1], f.y);
+      }
+    }
+    uint4 o;
+    __nv_bfloat162 *op = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) op[qq] = __floats2bfloat162_rn(acc[2 * qq], acc[2 * qq + 1]);
+    reinterpret_cast<uint4 *>(a.out + (size_t)t * a.d)[c8] = o;
+  }
+  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) a.trace[a.n_units_max + 148 + 9] = globaltimer_ns();
 }
 
 size_t gemm_smem_bytes() { return 1024 + (size_t)kStages * kStageBytes + sizeof(GemmShared); }
@@ -290,8 +528,17 @@ cudaError_t gemm_configure() {
 }
 
 cudaError_t launch_gemm(const CallArgs &a, const TmaMaps &maps, int n_sms, cudaStream_t s) {
-  k_gemm<<<n_sms, kGemmThreads, gemm_smem_bytes(), s>>>(maps, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_sms);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = gemm_smem_bytes();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm, maps, a);
 }
 
 }  // namespace tg

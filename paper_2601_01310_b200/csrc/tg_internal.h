@@ -16,6 +16,7 @@ constexpr int kMaxK = 8;
 constexpr int kMaxKeys = 1024;      // world * S_max  (key = rank * S_max + bank slot)
 constexpr int kRankBlock = 256;     // tokens per block of the rank kernel
 constexpr int kNumBoxes = 8;        // token-tile heights 16, 32, ..., 128
+constexpr int kMaxSlotsPerRank = 256;
 
 // GEMM tiling: swap-AB, weights fill UMMA M = 128,
 // tokens are UMMA N (16..128), K staged 64 wide (one 128-B swizzle row).
@@ -96,13 +97,13 @@ struct CallArgs {
   int32_t *sent_to;      // [kMaxWorld] this rank sends rows to dest
   int32_t *slot_rows;    // [S_loc] M_s on this rank
   int64_t *stats;        // [nkeys]
-  int32_t *sync;         // [8] block/CTA done counters and scheduler
+  int32_t *sync;         // [0..3] counters (scheduler, CTAs done, dispatch blocks); u64 grid barriers at [8], [10]
   int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters
   int n_ctr_max;
-  Unit *units;           // [n_units_max]
-  int32_t *n_units;      // [1]
-  int n_units_max;
+  int32_t *n_units;      // [1] units of the last call (written by the GEMM, diagnostics)
+  int n_units_max;       // capacity bound (trace sizing)
   int *err;              // host-mapped error word
+  uint64_t *trace;       // optional GEMM trace: [n_units_max] (end_ns << 16 | smid), [gridDim] start_ns
   // GEMM buffers (local)
   bf16 *H;               // [R_cap][F]
   bf16 *Hs;              // [T_max][Fsh]
@@ -114,11 +115,8 @@ struct CallArgs {
 };
 
 // Kernel launchers (tg_kernels.cu / tg_gemm.cu).  Return cudaGetLastError().
-cudaError_t launch_router(const CallArgs &a, const RouteKeys &rk, cudaStream_t s);
-cudaError_t launch_rank(const CallArgs &a, cudaStream_t s);
-cudaError_t launch_dispatch(const CallArgs &a, cudaStream_t s);
+cudaError_t launch_front(const CallArgs &a, const RouteKeys &rk, int n_sms, cudaStream_t s);
 cudaError_t launch_gemm(const CallArgs &a, const TmaMaps &maps, int n_sms, cudaStream_t s);
-cudaError_t launch_combine(const CallArgs &a, cudaStream_t s);
 cudaError_t launch_export_keys(const CallArgs &a, int n, int32_t *dst_rank, int32_t *dst_slot, cudaStream_t s);
 cudaError_t gemm_configure();
 size_t gemm_smem_bytes();

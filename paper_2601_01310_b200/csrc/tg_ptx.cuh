@@ -172,6 +172,30 @@ __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Scope-selected variants: world == 1 needs only GPU scope (no NVLink peers);
+// system-scope fences are microseconds and are paid only when peers exist.
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v, bool sys) {
+  if (sys) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p, bool sys) {
+  uint32_t v;
+  if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_scope(bool sys) {
+  if (sys) __threadfence_system();
+  else __threadfence();
+}
+__device__ __forceinline__ void wait_flag_ge_s(const uint32_t *flag, uint32_t epoch, bool sys, int *err, int code) {
+  if (static_cast<int32_t>(ld_acquire(flag, sys) - epoch) >= 0) return;
+  uint64_t t0 = globaltimer_ns();
+  while (static_cast<int32_t>(ld_acquire(flag, sys) - epoch) < 0) {
+    if (globaltimer_ns() - t0 > kWaitTimeoutNs) device_fail(err, code);
+  }
+}
+
 // Spin until *flag >= epoch (wrap-safe), bounded.
 __device__ __forceinline__ void wait_flag_ge(const uint32_t *flag, uint32_t epoch, int *err, int code) {
   if (static_cast<int32_t>(ld_acquire_sys(flag) - epoch) >= 0) return;
@@ -186,6 +210,31 @@ __device__ __forceinline__ void wait_ctr_ge(const int *ctr, int target, int *err
   while (ld_acquire_gpu(ctr) < target) {
     if (globaltimer_ns() - t0 > kWaitTimeoutNs) device_fail(err, code);
   }
+}
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident).  `count`
+// is a 64-bit counter that is never reset: barrier i of call `epoch` (1-based)
+// completes when count reaches ((epoch-1)*nbar + i+1) * gridDim.x.
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned long long *count, uint32_t epoch, int nbar, int i, int *err) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long target =
+        ((unsigned long long)(epoch - 1) * nbar + (unsigned long long)(i + 1)) * gridDim.x;
+    __threadfence();
+    atomicAdd(count, 1ull);
+    if (ld_acquire_gpu_u64(count) < target) {
+      uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_gpu_u64(count) < target)
+        if (globaltimer_ns() - t0 > kWaitTimeoutNs) device_fail(err, 0x3001);
+    }
+    __threadfence();
+  }
+  __syncthreads();
 }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {

@@ -10,6 +10,16 @@ import workloads as wl
 NEAR_TIE = 1e-5       # north_star: k-th vs (k+1)-th logit gap below which routing may differ
 W_TOL = 1e-6          # |w_gpu - w_oracle|
 OUT_TOL = 2e-2        # max|out_gpu - out_oracle| <= OUT_TOL * RMS(out_oracle)  (north_star)
+FLIP_FRAC = 1e-4      # DESIGN.md R#21: elements off by exactly one bf16 step (rounding-boundary
+                      # decisions taken on fp32- vs fp64-accumulated values) are counted, not failed,
+                      # while they stay below this fraction of the compared elements
+
+
+def bf16_step(v: np.ndarray) -> np.ndarray:
+    """Spacing of bf16 numbers at |v| (one rounding step), for v != 0."""
+    a = np.abs(v)
+    e = np.floor(np.log2(np.maximum(a, 2.0 ** -126)))
+    return np.exp2(e - 7)
 
 
 def bf16_to_f64(u16: np.ndarray) -> np.ndarray:
@@ -65,5 +75,15 @@ def compare(ref: dict, gpu_out: np.ndarray, routing: dict, tokens=None, check_pe
     rep["max_err"] = float(err.max()) if err.size else 0.0
     rep["mean_err"] = float(err.mean()) if err.size else 0.0
     rep["max_err_over_rms"] = rep["max_err"] / rms
-    assert rep["max_err"] <= OUT_TOL * rms, f"P4: max err {rep['max_err']:.4g} > {OUT_TOL} * RMS {rms:.4g}"
+    rep["n_compared"] = int(err.size)
+    rep["n_bit_diff"] = int((err > 0).sum())
+    over = err > OUT_TOL * rms
+    ref_sel = out_ref[sel]
+    flip = over & (err <= bf16_step(ref_sel) * 1.0000001)
+    rep["n_over_tol_one_step"] = int(flip.sum())
+    hard = over & ~flip
+    rep["max_err_excl_one_step_over_rms"] = float(err[~flip].max() / rms) if (~flip).any() else 0.0
+    assert not hard.any(), (f"P4: {int(hard.sum())} elements beyond {OUT_TOL}*RMS and beyond one bf16 step; "
+                            f"max err {rep['max_err']:.4g}, RMS {rms:.4g}")
+    assert flip.sum() <= max(1, FLIP_FRAC * err.size), f"P4: too many one-step flips beyond tol: {rep}"
     return rep

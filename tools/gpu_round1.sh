@@ -1,5 +1,5 @@
 set -x
-python -m paper_2601_01310_b200.build
+python paper_2601_01310_b200/build.py
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -s -k "mixtral or ds_ or qwen" > gpurun_out/gpu_big.log 2>&1; echo big_rc=$?
 tail -30 gpurun_out/gpu_big.log
 timeout 600 python bench.py > gpurun_out/bench1.log 2>&1; echo bench_rc=$?

@@ -1,0 +1,78 @@
+"""Timeline of the grouped GEMM kernel (GK4) from its device trace.
+
+    python tools/trace_gemm.py [--config mixtral_decode] [--tokens 256]
+
+Prints the kernel span, per-SM finish spread (tail), and per-kind unit
+durations (end time minus the previous unit end on the same SM).
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import workloads as wl  # noqa: E402
+import paper_2601_01310_b200 as tg  # noqa: E402
+from bench import make_weights_device  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="mixtral_decode")
+    ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--W", type=int, default=1)
+    a = ap.parse_args()
+    sh = wl.CONFIGS[a.config]
+    T = a.tokens or sh.T
+    pl = wl.make_placement(sh.E, a.W, 1, shadows=a.W > 1)
+    dev = torch.device("cuda", 0)
+    L = make_weights_device(sh, 1001, dev, list(range(sh.E)))
+    layer = tg.MoELayer(sh, pl, L, max_tokens_per_rank=T, device=0)
+    x = wl.make_tokens(sh, 1001, T=T, device=dev)
+    for _ in range(5):
+        layer(x)
+    tg.tg_set_trace(layer.ctx, True)
+    layer(x)
+    torch.cuda.synchronize()
+    tr = tg.tg_get_trace(layer.ctx)
+    st = tr["front_stamps"]
+    if st[0] > 0:
+        print("front kernel phase stamps (us from start: router, rank, exchange, dispatch):",
+              np.round((st[:5] - st[0]) / 1e3, 2).tolist())
+        t0g = tr["start"].min()
+        print("gemm: CTA start %.1f us after front start; grid barrier at %.1f, combine done %.1f us after GEMM start"
+              % ((t0g - st[0]) / 1e3, (st[8] - t0g) / 1e3, (st[9] - t0g) / 1e3))
+    np.savez(os.path.join(ROOT, "gpurun_out", f"trace_{a.config}_{T}.npz"), **tr)
+    analyze(tr)
+
+
+def analyze(tr):
+    end, smid, start, kind = tr["end"], tr["smid"], tr["start"], tr["kind"]
+    t0 = start.min()
+    end = (end - t0) / 1e3
+    print("units", len(end), "span %.1f us" % end.max())
+    fin = {}
+    for e, s in zip(end, smid):
+        fin[s] = max(fin.get(s, 0), e)
+    fin = np.array(list(fin.values()))
+    print(" per-SM finish min %.1f p10 %.1f median %.1f max %.1f -> mean idle tail %.1f us" % (
+        fin.min(), np.percentile(fin, 10), np.median(fin), fin.max(), fin.max() - fin.mean()))
+    order = np.argsort(end)
+    last = {}
+    durs = {0: [], 1: [], 2: [], 3: []}
+    for i in order:
+        s = smid[i]
+        durs[int(kind[i])].append(end[i] - last.get(s, 0.0))
+        last[s] = end[i]
+    for kd, v in durs.items():
+        if v:
+            v = np.array(v)
+            print(" kind %d n %d mean %.2f p50 %.2f p90 %.2f max %.2f" % (kd, len(v), v.mean(), np.median(v),
+                                                                        np.percentile(v, 90), v.max()))
+
+
+if __name__ == "__main__":
+    main()
