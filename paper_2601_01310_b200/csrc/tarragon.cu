@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -278,6 +279,10 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   a.ws = c->nsplit > 1 ? (float *)(sb + o_ws) : nullptr; a.ysh = Fsh > 0 ? (bf16 *)(sb + o_ysh) : nullptr;
   c->x_stage = (bf16 *)(sb + o_xs); c->out_stage = (bf16 *)(sb + o_os);
   a.L = L;
+  {
+    const char *e = getenv("TG_PDL");  // development switch for A/B timing; default on
+    a.pdl = (e && e[0] == '0') ? 0 : 1;
+  }
   CKI(cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
   *c->err_host = 0;
   CKI(cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));

@@ -207,6 +207,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tmem_alloc(&S->tmem_base, kTmemCols);
     tmem_relinquish();
   }
+  // PDL: the prologue above overlapped the front kernel; its outputs are read below
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 3) build_plan(a, S);
   tc_fence_before();
   __syncthreads();
@@ -470,6 +472,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // ===================== combine (GK5), all CTAs =====================
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 10);
   grid_barrier(gbar, a.epoch, 1, 0, err);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 8] = globaltimer_ns();
   if (blockIdx.x == 0 && threadIdx.x < a.world) {
     // every expert output this rank computed is in its source's combine buffer
@@ -533,11 +536,13 @@ cudaError_t launch_gemm(const CallArgs &a, const TmaMaps &maps, int n_sms, cudaS
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = gemm_smem_bytes();
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = a.pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k_gemm, maps, a);
 }
 

@@ -103,6 +103,7 @@ struct CallArgs {
   int32_t *n_units;      // [1] units of the last call (written by the GEMM, diagnostics)
   int n_units_max;       // capacity bound (trace sizing)
   int *err;              // host-mapped error word
+  int pdl;               // programmatic dependent launch between front and GEMM kernels
   uint64_t *trace;       // optional GEMM trace: [n_units_max] (end_ns << 16 | smid), [gridDim] start_ns
   // GEMM buffers (local)
   bf16 *H;               // [R_cap][F]

@@ -256,6 +256,8 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
                                                   const __grid_constant__ RouteKeys rk) {
   extern __shared__ __align__(16) uint8_t fsm[];
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8);
+  // PDL: everything below reads/writes state of the previous call's GEMM kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   TG_STAMP(0);
   // ---- P1 router (+ reset of the GEMM counters of this call)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
@@ -274,6 +276,8 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
   if (blockIdx.x == 0) exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(fsm));
   grid_barrier(gbar, a.epoch, kFrontBars, 2, a.err);
   TG_STAMP(3);
+  // the GEMM kernel may launch now: its prologue overlaps the dispatch
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- P4 dispatch: one warp per (token, j) pair
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -319,10 +323,11 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
   TG_STAMP(4);
 }
 
-// Tokens per router group: enough groups to cover the grid, TPB * E <= 1024.
+// Tokens per router group: the smallest power of two that needs one round of
+// groups over the grid (latency-bound), capped at 8 and TPB * E <= 1024.
 static int router_tpb(int T, int E, int nblk) {
-  int tpb = 8;
-  while (tpb > 1 && ((T + tpb - 1) / tpb < nblk || tpb * E > 1024)) tpb >>= 1;
+  int tpb = 1;
+  while (tpb < 8 && (T + tpb - 1) / tpb > nblk && 2 * tpb * E <= 1024) tpb <<= 1;
   return tpb;
 }
 
@@ -346,11 +351,13 @@ static cudaError_t launch_front_t(const CallArgs &a, const RouteKeys &rk, int nb
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = front_smem(a, TPB);
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = a.pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k_front<TPB>, a, rk);
 }
 

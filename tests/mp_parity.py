@@ -1,0 +1,152 @@
+"""Multi-GPU parity of tg_moe_layer (run under torchrun, one rank per GPU).
+
+    torchrun --nproc-per-node G --master-addr 127.0.0.1 --master-port P tests/mp_parity.py [--config tiny] [--W W]
+
+Every rank is an AW shard (contiguous token block) and hosts W/G logical EWs
+with spread shadows.  Checks: routing and the permutation of the
+rank's tokens bit-exact vs the oracle at G ranks, outputs within tolerance,
+masked EW (+ NaN poison) and route flips bit-identical, run-to-run bitwise,
+and (P7) the G-rank output bitwise equal to a 1-GPU run of the same layer.
+Rank 0 prints one JSON line with the report and exits non-zero on failure.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import workloads as wl  # noqa: E402
+from parity_util import compare, oracle_layer  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="tiny")
+    ap.add_argument("--W", type=int, default=0, help="logical EWs (default = world)")
+    ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--sample", type=int, default=0, help="oracle FFN on this many sampled tokens (0 = all)")
+    a = ap.parse_args()
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    import paper_2601_01310_b200 as tg
+
+    sh = wl.CONFIGS[a.config]
+    T = a.tokens or sh.T
+    assert T % world == 0
+    Tr = T // world
+    W = a.W or world
+    seed = 3000
+    L = wl.make_layer(sh, seed)
+    x = wl.make_tokens(sh, seed, T)
+    pl = wl.make_placement(sh.E, W, world)
+    layer = tg.MoELayer(sh, pl, L, max_tokens_per_rank=Tr, rank=rank, world=world, device=local,
+                        group=dist.group.WORLD)
+    xr = x[rank * Tr:(rank + 1) * Tr].contiguous().to(dev)
+    rep = {"rank": rank, "world": world, "W": W, "config": a.config, "T": T}
+    ok = True
+    msgs = []
+
+    def run():
+        o = layer(xr)
+        torch.cuda.synchronize()
+        return o
+
+    def gather(o):
+        outs = [torch.empty_like(o) for _ in range(world)]
+        dist.all_gather(outs, o)
+        return torch.cat(outs).cpu()
+
+    out = run()
+    rt = layer.routing(Tr)
+    out_all = gather(out)
+    # routing tensors of all ranks (rank order = global token order)
+    rt_all = {}
+    for kname in ("idx", "w", "dst_rank", "dst_slot", "dst_pos"):
+        t = rt[kname].contiguous()
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        rt_all[kname] = torch.cat(parts)
+    rt_all["counts"] = rt["counts"]
+    if rank == 0:
+        if a.sample:
+            rng = np.random.default_rng(seed)
+            tok = np.sort(rng.choice(T, size=min(a.sample, T), replace=False)).astype(np.int32)
+        else:
+            tok = None
+        ref = oracle_layer(L, x, pl, [0] * W, G=world, tokens=tok, n_threads=min(32, os.cpu_count() or 1))
+        try:
+            o_u16 = wl.as_u16(out_all)
+            rep["parity"] = compare(ref, o_u16 if tok is None else o_u16[tok], rt_all, tokens=tok)
+        except AssertionError as e:
+            ok = False
+            msgs.append(f"parity: {e}")
+    # determinism
+    out2 = run()
+    if not torch.equal(out.view(torch.int16), out2.view(torch.int16)):
+        ok = False
+        msgs.append(f"rank {rank}: run-to-run differs")
+    # mask EW1 (+ poison its slots on its rank) -> bit-identical
+    ew = 1 % W
+    layer.mask_worker(ew, 1)
+    if pl.ew_rank[ew] == rank:
+        nan = torch.full((sh.F, sh.d), float("nan"), dtype=torch.bfloat16, device=dev)
+        nan2 = torch.full((sh.d, sh.F), float("nan"), dtype=torch.bfloat16, device=dev)
+        for sl, e in enumerate(pl.hosted[ew]):
+            if e >= 0:
+                tg.tg_load_experts(layer.ctx, ew, sl, e, nan, nan, nan2)
+    else:
+        for sl, e in enumerate(pl.hosted[ew]):
+            if e >= 0:
+                tg.tg_load_experts(layer.ctx, ew, sl, e, None, None, None)
+    st0 = layer.stats()
+    dist.barrier()
+    out_m = run()
+    st1 = layer.stats() - st0
+    if not torch.equal(out.view(torch.int16), out_m.view(torch.int16)):
+        ok = False
+        msgs.append(f"rank {rank}: masked output differs ({int((out != out_m).sum())} elements)")
+    bank = [tg.tg_bank_slot(layer.ctx, w_, 0) for w_ in range(W)]
+    for sl in range(pl.slots_per_ew):
+        if st1[pl.ew_rank[ew], bank[ew] + sl] != 0:
+            ok = False
+            msgs.append(f"rank {rank}: masked EW received rows")
+    # rejoin is not possible after poisoning: flip to shadows-first with EW1 still masked
+    for i in range(4):
+        cand = wl.flipped(pl.cand) if i % 2 == 0 else pl.cand
+        layer.set_route_table(cand)
+        o = run()
+        if not torch.equal(out.view(torch.int16), o.view(torch.int16)):
+            ok = False
+            msgs.append(f"rank {rank}: flip {i} differs")
+    # P7: same layer on one GPU (rank 0), all tokens, W logical EWs
+    dist.barrier()
+    if rank == 0:
+        pl1 = wl.make_placement(sh.E, W, 1)
+        one = tg.MoELayer(sh, pl1, L, max_tokens_per_rank=T, rank=0, world=1, device=local)
+        o1 = one(x.to(dev))
+        torch.cuda.synchronize()
+        rep["cross_G_bit_identical"] = bool(torch.equal(o1.cpu().view(torch.int16), out_all.view(torch.int16)))
+        one.close()
+    flags = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flags)
+    if rank == 0:
+        rep["ok"] = bool(flags.item() == 0)
+        rep["errors"] = msgs
+        print(json.dumps(rep), flush=True)
+    layer.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if flags.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,38 @@
+"""Multi-GPU parity through torchrun (G = all visible GPUs, 2 or 4)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(G, *args):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + G), os.path.join(ROOT, "tests", "mp_parity.py"),
+           *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, f"rc={r.returncode}\n{r.stdout[-3000:]}\n{r.stderr[-3000:]}"
+    rep = json.loads(lines[-1])
+    print(rep)
+    assert rep["ok"], rep
+    return rep
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("W_mult", [1, 2])
+def test_tiny_multi_gpu(W_mult):
+    G = torch.cuda.device_count()
+    rep = _run(G, "--config", "tiny", "--W", str(G * W_mult))
+    assert rep["cross_G_bit_identical"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_mixtral_multi_gpu():
+    G = torch.cuda.device_count()
+    _run(G, "--config", "mixtral_decode", "--sample", "16")
