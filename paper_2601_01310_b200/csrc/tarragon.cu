@@ -251,6 +251,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t so = 0;
   auto carve = [&](size_t bytes) { size_t o = so; so = align_up(so + bytes, 256); return o; };
   size_t o_idx = carve(Tm * k * 4), o_w = carve(Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
+  size_t o_lp = carve(((Tm + 15) / 16) * ((size_t)(d + 511) / 512) * 16 * E * 4);
+  size_t o_gc2 = carve(((Tm + 15) / 16) * 4);
   size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
   size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
   size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(64);
@@ -270,7 +272,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   a.R_sh0 = c->R_sh0; a.nsplit = c->nsplit;
   a.wg = c->wg;
   a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.key = (int32_t *)(sb + o_key);
-  a.lrank = (int32_t *)(sb + o_lrank); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
+  a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
   a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
   a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
   a.sync = (int32_t *)(sb + o_sync); a.ctr = (int32_t *)(sb + o_ctr);

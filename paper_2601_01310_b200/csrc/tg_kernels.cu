@@ -1,8 +1,9 @@
 // tg_kernels.cu — GK1-3 "front" kernel of the MoE round trip (AW side, then the
 // dispatch exchange), one cooperative launch with grid barriers between phases:
 //
-//   P1 router   : fp32 router logits, top-k (lowest id on ties), softmax over
-//                 the k selected, ERT resolve -> destination key per pair
+//   P1 router   : router logits on tensor cores (bf16 x bf16 -> fp32), top-k
+//                 (lowest id on ties), softmax over the k selected, ERT
+//                 resolve -> destination key per pair
 //                 (§2.1; §4.2; §5.1).
 //   P2 rank     : stable rank of every (token, j) pair among this rank's pairs
 //                 with the same destination key, in token order (per-chunk
@@ -30,126 +31,179 @@ constexpr int kFrontBars = 3;  // grid barriers per front call
   } while (0)
 
 // --------------------------------------------------------------------- P1
-// TPB tokens per group; warp w reduces the d-slice [w*d/8, (w+1)*d/8) of
-// x . Wg[e] for all TPB tokens and all experts: lanes accumulate their 16-B
-// chunks with fp32 FMA (bf16 products are exact in fp32), a fixed xor
-// butterfly reduces the 32 lanes and the 8 warp partials are summed in warp
-// order.  A token's logit reduction tree depends only on d — never on T, TPB
-// or its position — so routing is deterministic and row-invariant.
-template <int TPB>
-__device__ void router_group(const CallArgs &a, const RouteKeys &rk, int t0, float *part) {
+// Router logits on tensor cores.  Work item = (16-token group, K part of
+// kKPart = 512 elements); warp w of the block reduces 64 elements of the part
+// with mma.sync.m16n8k16 (bf16 in, fp32 accumulate; bf16 products are exact),
+// the 8 warp partials are summed in warp order and the part's partial logits go
+// to global memory; P2 sums the parts in part order.  The reduction tree of a
+// logit depends only on d — never on T, the token's group or its row — so
+// routing is deterministic and row-invariant.  Experts in 64-wide groups.
+constexpr int kRouterRows = 16;
+constexpr int kKPart = 512;
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ int router_kparts(int d) { return (d + kKPart - 1) / kKPart; }
+
+__device__ void topk_token(const CallArgs &a, const RouteKeys &rk, int t, const float *lg);
+
+// partial logits of group `grp`, K part `kp` -> a.logit_part[(grp * nkp + kp) * 16 * E + row * E + e];
+// the last of the nkp items of a group to finish sums the parts in part order and
+// runs the top-k of the group's 16 tokens.
+__device__ void router_item(const CallArgs &a, const RouteKeys &rk, int grp, int kp, float *part) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = a.d, E = a.E, k = a.k, T = a.T;
-  const int nch = d >> 3;
-  const int cw = nch >> 3;
-  const int c_lo = warp * cw, c_hi = c_lo + cw;
-  const uint4 *xr[TPB];
+  const int d = a.d, E = a.E, T = a.T;
+  const int g = lane >> 2, c = lane & 3;
+  const int t0 = grp * kRouterRows;
+  const int kb = kp * kKPart + warp * (kKPart / 8);  // this warp's 64 K elements
+  const int nkp = router_kparts(d);
+  const bool active = kb < d;
+  const uint32_t *xr0 = reinterpret_cast<const uint32_t *>(a.x + (size_t)min(t0 + g, T - 1) * d);
+  const uint32_t *xr1 = reinterpret_cast<const uint32_t *>(a.x + (size_t)min(t0 + g + 8, T - 1) * d);
+  uint32_t af[4][4];
+  if (active) {
 #pragma unroll
-  for (int t = 0; t < TPB; ++t) xr[t] = reinterpret_cast<const uint4 *>(a.x + (size_t)min(t0 + t, T - 1) * d);
-  for (int e0 = 0; e0 < E; e0 += 8) {
-    float acc[TPB][8];
+    for (int s = 0; s < 4; ++s) {
+      const int o0 = ((kb + 16 * s) >> 1) + c, o1 = o0 + 4;  // uint32 offsets of cols 2c and 2c+8
+      af[s][0] = __ldg(xr0 + o0);
+      af[s][1] = __ldg(xr1 + o0);
+      af[s][2] = __ldg(xr0 + o1);
+      af[s][3] = __ldg(xr1 + o1);
+    }
+  }
+  for (int e0 = 0; e0 < E; e0 += 64) {
+    float acc[8][4];
 #pragma unroll
-    for (int t = 0; t < TPB; ++t)
+    for (int n = 0; n < 8; ++n)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[t][i] = 0.f;
-    for (int c = c_lo + lane; c < c_hi; c += 32) {
-      uint4 wv[8];
+      for (int i = 0; i < 4; ++i) acc[n][i] = 0.f;
+    if (active) {
+      uint32_t bf[8][4][2];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        wv[i] = (e0 + i < E) ? __ldg(reinterpret_cast<const uint4 *>(a.wg + (size_t)(e0 + i) * d) + c)
-                             : make_uint4(0, 0, 0, 0);
+      for (int n = 0; n < 8; ++n) {
+        const uint32_t *wr = reinterpret_cast<const uint32_t *>(a.wg + (size_t)min(e0 + 8 * n + g, E - 1) * d);
 #pragma unroll
-      for (int t = 0; t < TPB; ++t) {
-        uint4 xv = __ldg(xr[t] + c);
-        const __nv_bfloat162 *xp = reinterpret_cast<const __nv_bfloat162 *>(&xv);
-        float2 xf[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) xf[q] = __bfloat1622float2(xp[q]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const __nv_bfloat162 *wp = reinterpret_cast<const __nv_bfloat162 *>(&wv[i]);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float2 wf = __bfloat1622float2(wp[q]);
-            acc[t][i] = __fmaf_rn(xf[q].x, wf.x, acc[t][i]);
-            acc[t][i] = __fmaf_rn(xf[q].y, wf.y, acc[t][i]);
-          }
+        for (int s = 0; s < 4; ++s) {
+          const int o0 = ((kb + 16 * s) >> 1) + c;
+          bf[n][s][0] = (e0 + 8 * n < E) ? __ldg(wr + o0) : 0u;
+          bf[n][s][1] = (e0 + 8 * n < E) ? __ldg(wr + o0 + 4) : 0u;
         }
       }
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+          if (e0 + 8 * n < E) mma_bf16_16816(acc[n], af[s], bf[n][s][0], bf[n][s][1]);
     }
 #pragma unroll
-    for (int t = 0; t < TPB; ++t)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float v = acc[t][i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0 && e0 + i < E) part[(warp * TPB + t) * E + e0 + i] = v;
+    for (int n = 0; n < 8; ++n) {
+      float *p = part + (warp * kRouterRows) * 64 + 8 * n + 2 * c;
+      p[g * 64] = acc[n][0];
+      p[g * 64 + 1] = acc[n][1];
+      p[(g + 8) * 64] = acc[n][2];
+      p[(g + 8) * 64 + 1] = acc[n][3];
+    }
+    __syncthreads();
+    float *dst = a.logit_part + ((size_t)grp * nkp + kp) * kRouterRows * E;
+    for (int i = threadIdx.x; i < kRouterRows * 64; i += blockDim.x) {
+      const int r = i >> 6, e = e0 + (i & 63);
+      if (e < E) {
+        float s = part[i];
+        for (int ww = 1; ww < 8; ++ww) s += part[ww * kRouterRows * 64 + i];
+        dst[r * E + e] = s;
       }
+    }
+    __syncthreads();
+  }
+  // ---- last K part of this group: final logits (parts summed in order) + top-k
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int old = atomicAdd(reinterpret_cast<unsigned int *>(a.grp_ctr) + grp, 1u);
+    s_last = (old + 1u == (unsigned)nkp);  // counters are zeroed in P2 of every call
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < TPB * E; i += blockDim.x) {
-    float s = part[i];
-    for (int ww = 1; ww < 8; ++ww) s += part[ww * TPB * E + i];
-    part[i] = s;  // logit of token t0 + i / E, expert i % E
+  if (!s_last) return;
+  __threadfence();
+  float *lg = part;  // [16][E]
+  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * E;
+  for (int i = threadIdx.x; i < kRouterRows * E; i += blockDim.x) {
+    float s = __ldcg(src + i);
+    for (int q = 1; q < nkp; ++q) s += __ldcg(src + (size_t)q * kRouterRows * E + i);
+    lg[i] = s;
   }
   __syncthreads();
-  const int t = t0 + warp;
-  if (warp < TPB && t < T) {
-    const float *lg = part + warp * E;
-    // top-k: k rounds of warp argmax on (value desc, id asc); -0 == +0 ties
-    uint32_t taken = 0;  // bit i: expert lane + 32 i already selected
-    int sel[kMaxK];
-    float sv[kMaxK];
-    for (int r = 0; r < k; ++r) {
-      float bv = -INFINITY;
-      int bi = 0x7fffffff;
-      for (int i = 0; lane + 32 * i < E; ++i) {
-        int e = lane + 32 * i;
-        if (taken & (1u << i)) continue;
-        float v = lg[e];
-        if (v > bv || (v == bv && e < bi)) { bv = v; bi = e; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-      }
-      sel[r] = bi;
-      sv[r] = bv;
-      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-    }
-    if (lane == 0) {
-      // slots in ascending expert id (R#4)
-      for (int q = 1; q < k; ++q) {
-        int ve = sel[q];
-        float vv = sv[q];
-        int b = q - 1;
-        while (b >= 0 && sel[b] > ve) { sel[b + 1] = sel[b]; sv[b + 1] = sv[b]; --b; }
-        sel[b + 1] = ve;
-        sv[b + 1] = vv;
-      }
-      float m = sv[0];
-      for (int j = 1; j < k; ++j) m = fmaxf(m, sv[j]);
-      float z[kMaxK], Z = 0.f;
-      for (int j = 0; j < k; ++j) { z[j] = expf(sv[j] - m); Z = Z + z[j]; }
-      for (int j = 0; j < k; ++j) {
-        a.idx[(size_t)t * k + j] = sel[j];
-        a.w[(size_t)t * k + j] = __fdiv_rn(z[j], Z);
-        a.key[(size_t)t * k + j] = rk.key[sel[j]];
-      }
-    }
-  }
-  __syncthreads();  // part[] is reused by the next group
+  for (int rr = warp; rr < kRouterRows; rr += 8)
+    if (t0 + rr < T) topk_token(a, rk, t0 + rr, lg + rr * E);
+  __syncthreads();
 }
 
 // --------------------------------------------------------------------- P2
-// Chunk of 256 tokens: bit t of bm[K][t/32] is set iff token t has a pair with
-// key K (at most one per token: its k experts are distinct and map to distinct
-// slots).  The rank of (t, K) in the chunk is the popcount of the bits below t.
-__device__ void rank_chunk(const CallArgs &a, int chunk, uint32_t *bm) {
+// Chunk of 256 tokens.  (a) each warp finishes 32 tokens: logits = sum of the K
+// parts in part order, top-k by k rounds of warp argmax on (value desc, id asc;
+// -0 == +0 ties), slots in ascending expert id (R#4), softmax over the k
+// selected (IEEE expf / div), ERT key.  (b) bit t of bm[K][t/32] is set iff
+// token t has a pair with key K (at most one per token: its k experts are
+// distinct and map to distinct slots); the rank of (t, K) in the chunk is the
+// popcount of the bits below t.
+__device__ void topk_token(const CallArgs &a, const RouteKeys &rk, int t, const float *lg) {
+  const int lane = threadIdx.x & 31;
+  const int E = a.E, k = a.k;
+  uint32_t taken = 0;  // bit i: expert lane + 32 i already selected
+  int sel[kMaxK];
+  float sv[kMaxK];
+  for (int r = 0; r < k; ++r) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = 0; lane + 32 * i < E; ++i) {
+      int e = lane + 32 * i;
+      if (taken & (1u << i)) continue;
+      float v = lg[e];
+      if (v > bv || (v == bv && e < bi)) { bv = v; bi = e; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    sel[r] = bi;
+    sv[r] = bv;
+    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+  }
+  if (lane == 0) {
+    for (int q = 1; q < k; ++q) {
+      int ve = sel[q];
+      float vv = sv[q];
+      int b = q - 1;
+      while (b >= 0 && sel[b] > ve) { sel[b + 1] = sel[b]; sv[b + 1] = sv[b]; --b; }
+      sel[b + 1] = ve;
+      sv[b + 1] = vv;
+    }
+    float m = sv[0];
+    for (int j = 1; j < k; ++j) m = fmaxf(m, sv[j]);
+    float z[kMaxK], Z = 0.f;
+    for (int j = 0; j < k; ++j) { z[j] = expf(sv[j] - m); Z = Z + z[j]; }
+    for (int j = 0; j < k; ++j) {
+      const int key = rk.key[sel[j]];
+      a.idx[(size_t)t * k + j] = sel[j];
+      a.w[(size_t)t * k + j] = __fdiv_rn(z[j], Z);
+      a.key[(size_t)t * k + j] = key;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ void rank_chunk(const CallArgs &a, int chunk, uint8_t *smraw) {
   const int tid = threadIdx.x, nkeys = a.nkeys, k = a.k;
+  uint32_t *bm = reinterpret_cast<uint32_t *>(smraw);  // [nkeys][8]
   const int t = chunk * kRankBlock + tid;
   for (int i = tid; i < nkeys * 8; i += blockDim.x) bm[i] = 0;
   __syncthreads();
@@ -251,7 +305,6 @@ __device__ __forceinline__ void copy_row(uint4 *__restrict__ dst, const uint4 *_
   for (; c < nch; c += 32) dst[c] = __ldg(src + c);
 }
 
-template <int TPB>
 __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallArgs a,
                                                   const __grid_constant__ RouteKeys rk) {
   extern __shared__ __align__(16) uint8_t fsm[];
@@ -262,14 +315,16 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
   // ---- P1 router (+ reset of the GEMM counters of this call)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x < 4) a.sync[threadIdx.x] = 0;
-  const int ngroups = (a.T + TPB - 1) / TPB;
-  for (int g = blockIdx.x; g < ngroups; g += gridDim.x)
-    router_group<TPB>(a, rk, g * TPB, reinterpret_cast<float *>(fsm));
+  const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
+  const int nkp = router_kparts(a.d);
+  for (int it = blockIdx.x; it < ngroups * nkp; it += gridDim.x)
+    router_item(a, rk, it / nkp, it % nkp, reinterpret_cast<float *>(fsm));
   grid_barrier(gbar, a.epoch, kFrontBars, 0, a.err);
   TG_STAMP(1);
-  // ---- P2 rank
+  // ---- P2 rank (+ reset of the router group counters for the next call)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ngroups; i += gridDim.x * blockDim.x) a.grp_ctr[i] = 0;
   const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
-  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, reinterpret_cast<uint32_t *>(fsm));
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, fsm);
   grid_barrier(gbar, a.epoch, kFrontBars, 1, a.err);
   TG_STAMP(2);
   // ---- P3 counts exchange + layout (block 0)
@@ -323,33 +378,24 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
   TG_STAMP(4);
 }
 
-// Tokens per router group: the smallest power of two that needs one round of
-// groups over the grid (latency-bound), capped at 8 and TPB * E <= 1024.
-static int router_tpb(int T, int E, int nblk) {
-  int tpb = 1;
-  while (tpb < 8 && (T + tpb - 1) / tpb > nblk && 2 * tpb * E <= 1024) tpb <<= 1;
-  return tpb;
-}
-
-static size_t front_smem(const CallArgs &a, int tpb) {
-  size_t r = sizeof(float) * 8 * tpb * a.E;
+static size_t front_smem(const CallArgs &a) {
+  size_t r = sizeof(float) * std::max(8 * kRouterRows * 64, kRouterRows * a.E);
   size_t b = sizeof(uint32_t) * 8 * a.nkeys;
   size_t e = sizeof(int32_t) * 3 * a.nkeys;
   return std::max(r, std::max(b, e));
 }
 
-template <int TPB>
-static cudaError_t launch_front_t(const CallArgs &a, const RouteKeys &rk, int nblk, cudaStream_t s) {
+cudaError_t launch_front(const CallArgs &a, const RouteKeys &rk, int n_sms, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_front<TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nblk);
+  cfg.gridDim = dim3(n_sms);
   cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = front_smem(a, TPB);
+  cfg.dynamicSmemBytes = front_smem(a);
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
@@ -358,17 +404,7 @@ static cudaError_t launch_front_t(const CallArgs &a, const RouteKeys &rk, int nb
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = a.pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k_front<TPB>, a, rk);
-}
-
-cudaError_t launch_front(const CallArgs &a, const RouteKeys &rk, int n_sms, cudaStream_t s) {
-  const int nblk = n_sms;
-  switch (router_tpb(a.T, a.E, nblk)) {
-    case 8: return launch_front_t<8>(a, rk, nblk, s);
-    case 4: return launch_front_t<4>(a, rk, nblk, s);
-    case 2: return launch_front_t<2>(a, rk, nblk, s);
-    default: return launch_front_t<1>(a, rk, nblk, s);
-  }
+  return cudaLaunchKernelEx(&cfg, k_front, a, rk);
 }
 
 // Parity export: destination key -> (rank, bank slot) of every pair of the last call.
