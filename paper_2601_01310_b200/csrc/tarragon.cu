@@ -251,8 +251,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t so = 0;
   auto carve = [&](size_t bytes) { size_t o = so; so = align_up(so + bytes, 256); return o; };
   size_t o_idx = carve(Tm * k * 4), o_w = carve(Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
-  size_t o_lp = carve(((Tm + 15) / 16) * ((size_t)(d + 511) / 512) * 16 * E * 4);
-  size_t o_gc2 = carve(((Tm + 15) / 16) * 4);
+  size_t o_lp = carve(((Tm + 31) / 32) * (size_t)(d / 64) * 32 * E * 4);  // groups * nkp * 32 * E floats (KP >= 64)
+  size_t o_gc2 = carve(((Tm + 31) / 32) * 4);
   size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
   size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
   size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(64);
@@ -576,8 +576,8 @@ tg_status tg_set_trace(tg_ctx *c, int on) {
   if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
   CK(cudaSetDevice(c->device));
   if (on && !c->trace) {
-    CK(cudaMalloc(&c->trace, sizeof(uint64_t) * ((size_t)c->args.n_units_max + 148 + 64)));
-    CK(cudaMemset(c->trace, 0, sizeof(uint64_t) * ((size_t)c->args.n_units_max + 148 + 64)));
+    CK(cudaMalloc(&c->trace, sizeof(uint64_t) * ((size_t)c->args.n_units_max + 148 + 64 + 1024)));
+    CK(cudaMemset(c->trace, 0, sizeof(uint64_t) * ((size_t)c->args.n_units_max + 148 + 64 + 1024)));
   }
   c->tracing = on != 0;
   return TG_OK;
@@ -592,10 +592,10 @@ tg_status tg_get_trace(tg_ctx *c, uint64_t *trace, int cap, int *n_units, int *n
   CK(cudaMemcpy(&nu, c->args.n_units, sizeof(int), cudaMemcpyDeviceToHost));
   *n_units = nu;
   *n_ctas = c->n_sms;
-  if (nu + 148 + 64 > cap) return fail(c, TG_ERR_INVALID, "trace capacity %d < %d", cap, nu + 148 + 64);
+  if (nu + 148 + 64 + 1024 > cap) return fail(c, TG_ERR_INVALID, "trace capacity %d < %d", cap, nu + 148 + 64 + 1024);
   if (trace) {
     CK(cudaMemcpy(trace, c->trace, sizeof(uint64_t) * nu, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(trace + nu, c->trace + c->args.n_units_max, sizeof(uint64_t) * (148 + 64), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(trace + nu, c->trace + c->args.n_units_max, sizeof(uint64_t) * (148 + 64 + 1024), cudaMemcpyDeviceToHost));
   }
   return check_sticky(c);
 }

@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 10);
   grid_barrier(gbar, a.epoch, 1, 0, err);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 8] = globaltimer_ns();
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 16] = globaltimer_ns();
   if (blockIdx.x == 0 && threadIdx.x < a.world) {
     // every expert output this rank computed is in its source's combine buffer
     fence_scope(sys);
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int qq = 0; qq < 4; ++qq) op[qq] = __floats2bfloat162_rn(acc[2 * qq], acc[2 * qq + 1]);
     reinterpret_cast<uint4 *>(a.out + (size_t)t * a.d)[c8] = o;
   }
-  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) a.trace[a.n_units_max + 148 + 9] = globaltimer_ns();
+  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) a.trace[a.n_units_max + 148 + 17] = globaltimer_ns();
 }
 
 size_t gemm_smem_bytes() { return 1024 + (size_t)kStages * kStageBytes + sizeof(GemmShared); }

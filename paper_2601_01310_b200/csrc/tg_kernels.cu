@@ -1,9 +1,11 @@
 // tg_kernels.cu — GK1-3 "front" kernel of the MoE round trip (AW side, then the
 // dispatch exchange), one cooperative launch with grid barriers between phases:
 //
-//   P1 router   : router logits on tensor cores (bf16 x bf16 -> fp32), top-k
-//                 (lowest id on ties), softmax over the k selected, ERT
-//                 resolve -> destination key per pair
+//   P1 router   : router logits on tensor cores (bf16 x bf16 -> fp32), K split
+//                 in parts fixed by (d, E), partial logits to global memory
+//   P1b top-k   : one warp per token: parts summed in order, top-k (lowest id
+//                 on ties), softmax over the k selected, ERT resolve ->
+//                 destination key per pair
 //                 (§2.1; §4.2; §5.1).
 //   P2 rank     : stable rank of every (token, j) pair among this rank's pairs
 //                 with the same destination key, in token order (per-chunk
@@ -22,7 +24,7 @@
 
 namespace tg {
 
-constexpr int kFrontBars = 3;  // grid barriers per front call
+constexpr int kFrontBars = 4;  // grid barriers per front call
 
 #define TG_STAMP(i)                                                                     \
   do {                                                                                  \
@@ -31,15 +33,18 @@ constexpr int kFrontBars = 3;  // grid barriers per front call
   } while (0)
 
 // --------------------------------------------------------------------- P1
-// Router logits on tensor cores.  Work item = (16-token group, K part of
-// kKPart = 512 elements); warp w of the block reduces 64 elements of the part
-// with mma.sync.m16n8k16 (bf16 in, fp32 accumulate; bf16 products are exact),
-// the 8 warp partials are summed in warp order and the part's partial logits go
-// to global memory; P2 sums the parts in part order.  The reduction tree of a
-// logit depends only on d — never on T, the token's group or its row — so
-// routing is deterministic and row-invariant.  Experts in 64-wide groups.
-constexpr int kRouterRows = 16;
-constexpr int kKPart = 512;
+// Router logits on tensor cores.  The K dimension is cut into parts of KP
+// elements (a function of d and E only); block b owns part kp = b % nkp for
+// the whole phase and stages the Wg slice [E][KP] in shared memory once (rows
+// padded by 16 B: conflict-free fragment loads).  Work item = (32-token group,
+// part): the x tile [32][KP] is staged with coalesced 16-B loads, warp w
+// reduces KP/8 elements with mma.sync.m16n8k16 (bf16 in, fp32 accumulate;
+// bf16 products are exact), k16 steps in order, the 8 warp partials are summed
+// in warp order and written to global memory; the last part of a group to
+// arrive sums the parts in part order and runs the top-k.  The reduction tree
+// of a logit depends only on (d, E) — never on T, the token's group or its row
+// — so routing is deterministic and row-invariant.
+constexpr int kRouterRows = 32;
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -49,153 +54,216 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ int router_kparts(int d) { return (d + kKPart - 1) / kKPart; }
+__host__ __device__ __forceinline__ int router_kpart(int d, int E) {
+  int kp = E <= 96 ? 512 : (E <= 192 ? 256 : 128);
+  while (kp > 64 && d % kp) kp >>= 1;  // d % 64 == 0, so 64 always divides d
+  return kp;
+}
+__host__ __device__ __forceinline__ int router_nkp(int d, int E) { return (d + router_kpart(d, E) - 1) / router_kpart(d, E); }
+__host__ __device__ __forceinline__ int router_epad(int E) { return (E + 63) / 64 * 64; }
 
-__device__ void topk_token(const CallArgs &a, const RouteKeys &rk, int t, const float *lg);
 
-// partial logits of group `grp`, K part `kp` -> a.logit_part[(grp * nkp + kp) * 16 * E + row * E + e];
-// the last of the nkp items of a group to finish sums the parts in part order and
-// runs the top-k of the group's 16 tokens.
-__device__ void router_item(const CallArgs &a, const RouteKeys &rk, int grp, int kp, float *part) {
+struct RouterSmem {
+  uint32_t *wg;   // [Epad][KP/2 + 4] words
+  uint32_t *xt;   // [32][KP/2 + 4] words
+  float *part;    // [8][32][64]
+  int ldw;        // row stride in words
+};
+
+// Batched copy of rows of 16-B chunks into padded smem rows: 8 loads in flight per
+// thread before the stores (these loops are latency-bound, not bandwidth-bound).
+template <typename RowPtr>
+__device__ __forceinline__ void stage_rows(uint32_t *dst, int ldw, int nrows, int cpr, RowPtr row) {
+  const int total = nrows * cpr;
+  for (int i0 = threadIdx.x; i0 < total; i0 += 8 * blockDim.x) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      const uint4 *p = (i < total) ? row(i / cpr) : nullptr;
+      v[u] = p ? __ldg(p + i % cpr) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < total) *reinterpret_cast<uint4 *>(dst + (i / cpr) * ldw + (i % cpr) * 4) = v[u];
+    }
+  }
+}
+
+__device__ void router_stage_wg(const CallArgs &a, const RouterSmem &R, int kp) {
+  const int KP = router_kpart(a.d, a.E);
+  const int E8 = (a.E + 7) / 8 * 8;  // rows of the n8 tiles actually used
+  stage_rows(R.wg, R.ldw, E8, KP / 8, [&](int e) -> const uint4 * {
+    return e < a.E ? reinterpret_cast<const uint4 *>(a.wg + (size_t)e * a.d + kp * KP) : nullptr;
+  });
+}
+
+__device__ void router_item(const CallArgs &a, const RouteKeys &rk, const RouterSmem &R, int grp, int kp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = a.d, E = a.E, T = a.T;
   const int g = lane >> 2, c = lane & 3;
+  const int KP = router_kpart(d, E), nkp = router_nkp(d, E), Epad = router_epad(E);
   const int t0 = grp * kRouterRows;
-  const int kb = kp * kKPart + warp * (kKPart / 8);  // this warp's 64 K elements
-  const int nkp = router_kparts(d);
-  const bool active = kb < d;
-  const uint32_t *xr0 = reinterpret_cast<const uint32_t *>(a.x + (size_t)min(t0 + g, T - 1) * d);
-  const uint32_t *xr1 = reinterpret_cast<const uint32_t *>(a.x + (size_t)min(t0 + g + 8, T - 1) * d);
-  uint32_t af[4][4];
-  if (active) {
+  const int cpr = KP / 8;
+  if (grp == 0 && kp == 0) TG_STAMP(10);
+  // x tile [32][KP] -> smem (rows past T clamped; their results are never used)
+  stage_rows(R.xt, R.ldw, kRouterRows, cpr, [&](int r) -> const uint4 * {
+    return reinterpret_cast<const uint4 *>(a.x + (size_t)min(t0 + r, T - 1) * d + kp * KP);
+  });
+  __syncthreads();
+  if (grp == 0 && kp == 0) TG_STAMP(11);
+  const int ksw = max(16, KP / 8);   // K elements of this warp (multiple of 16)
+  const int nsteps = (warp * ksw < KP) ? ksw / 16 : 0;
+  const int wk0 = warp * ksw / 2;    // first word column
+  float *dst = a.logit_part + ((size_t)grp * nkp + kp) * kRouterRows * E;
+  for (int e0 = 0; e0 < Epad; e0 += 64) {
+    const int ntr = min(8, (E - e0 + 7) / 8);  // n8 tiles holding real experts
+    float acc[2][8][4];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int o0 = ((kb + 16 * s) >> 1) + c, o1 = o0 + 4;  // uint32 offsets of cols 2c and 2c+8
-      af[s][0] = __ldg(xr0 + o0);
-      af[s][1] = __ldg(xr1 + o0);
-      af[s][2] = __ldg(xr0 + o1);
-      af[s][3] = __ldg(xr1 + o1);
-    }
-  }
-  for (int e0 = 0; e0 < E; e0 += 64) {
-    float acc[8][4];
+    for (int m = 0; m < 2; ++m)
 #pragma unroll
-    for (int n = 0; n < 8; ++n)
+      for (int n = 0; n < 8; ++n)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[n][i] = 0.f;
-    if (active) {
-      uint32_t bf[8][4][2];
+        for (int i = 0; i < 4; ++i) acc[m][n][i] = 0.f;
+    for (int s = 0; s < nsteps; ++s) {
+      const int wc = wk0 + 8 * s + c;  // word column of k = 16 s + 2 c
+      uint32_t af[2][4];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const uint32_t *x0 = R.xt + (16 * m + g) * R.ldw, *x1 = x0 + 8 * R.ldw;
+        af[m][0] = x0[wc];
+        af[m][1] = x1[wc];
+        af[m][2] = x0[wc + 4];
+        af[m][3] = x1[wc + 4];
+      }
 #pragma unroll
       for (int n = 0; n < 8; ++n) {
-        const uint32_t *wr = reinterpret_cast<const uint32_t *>(a.wg + (size_t)min(e0 + 8 * n + g, E - 1) * d);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const int o0 = ((kb + 16 * s) >> 1) + c;
-          bf[n][s][0] = (e0 + 8 * n < E) ? __ldg(wr + o0) : 0u;
-          bf[n][s][1] = (e0 + 8 * n < E) ? __ldg(wr + o0 + 4) : 0u;
+        if (n < ntr) {
+          const uint32_t *wr = R.wg + (e0 + 8 * n + g) * R.ldw;
+          const uint32_t b0 = wr[wc], b1 = wr[wc + 4];
+          mma_bf16_16816(acc[0][n], af[0], b0, b1);
+          mma_bf16_16816(acc[1][n], af[1], b0, b1);
         }
       }
-#pragma unroll
-      for (int s = 0; s < 4; ++s)
-#pragma unroll
-        for (int n = 0; n < 8; ++n)
-          if (e0 + 8 * n < E) mma_bf16_16816(acc[n], af[s], bf[n][s][0], bf[n][s][1]);
     }
 #pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      float *p = part + (warp * kRouterRows) * 64 + 8 * n + 2 * c;
-      p[g * 64] = acc[n][0];
-      p[g * 64 + 1] = acc[n][1];
-      p[(g + 8) * 64] = acc[n][2];
-      p[(g + 8) * 64 + 1] = acc[n][3];
-    }
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        if (n >= ntr) continue;
+        float *p = R.part + (warp * kRouterRows + 16 * m) * 64 + 8 * n + 2 * c;
+        p[g * 64] = acc[m][n][0];
+        p[g * 64 + 1] = acc[m][n][1];
+        p[(g + 8) * 64] = acc[m][n][2];
+        p[(g + 8) * 64 + 1] = acc[m][n][3];
+      }
     __syncthreads();
-    float *dst = a.logit_part + ((size_t)grp * nkp + kp) * kRouterRows * E;
-    for (int i = threadIdx.x; i < kRouterRows * 64; i += blockDim.x) {
-      const int r = i >> 6, e = e0 + (i & 63);
-      if (e < E) {
-        float s = part[i];
-        for (int ww = 1; ww < 8; ++ww) s += part[ww * kRouterRows * 64 + i];
-        dst[r * E + e] = s;
+    const int ew = min(64, E - e0);
+    for (int i = threadIdx.x; i < kRouterRows * ew; i += blockDim.x) {
+      const int r = i / ew, ee = i % ew, e = e0 + ee;
+      {
+        const int pi = r * 64 + ee;
+        float sum = R.part[pi];
+#pragma unroll
+        for (int ww = 1; ww < 8; ++ww) sum += R.part[ww * kRouterRows * 64 + pi];
+        dst[r * E + e] = sum;
       }
     }
     __syncthreads();
   }
-  // ---- last K part of this group: final logits (parts summed in order) + top-k
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int old = atomicAdd(reinterpret_cast<unsigned int *>(a.grp_ctr) + grp, 1u);
-    s_last = (old + 1u == (unsigned)nkp);  // counters are zeroed in P2 of every call
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  float *lg = part;  // [16][E]
-  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * E;
-  for (int i = threadIdx.x; i < kRouterRows * E; i += blockDim.x) {
-    float s = __ldcg(src + i);
-    for (int q = 1; q < nkp; ++q) s += __ldcg(src + (size_t)q * kRouterRows * E + i);
-    lg[i] = s;
-  }
-  __syncthreads();
-  for (int rr = warp; rr < kRouterRows; rr += 8)
-    if (t0 + rr < T) topk_token(a, rk, t0 + rr, lg + rr * E);
-  __syncthreads();
 }
 
 // --------------------------------------------------------------------- P2
-// Chunk of 256 tokens.  (a) each warp finishes 32 tokens: logits = sum of the K
-// parts in part order, top-k by k rounds of warp argmax on (value desc, id asc;
-// -0 == +0 ties), slots in ascending expert id (R#4), softmax over the k
-// selected (IEEE expf / div), ERT key.  (b) bit t of bm[K][t/32] is set iff
+// Chunk of 256 tokens: bit t of bm[K][t/32] is set iff
 // token t has a pair with key K (at most one per token: its k experts are
 // distinct and map to distinct slots); the rank of (t, K) in the chunk is the
 // popcount of the bits below t.
-__device__ void topk_token(const CallArgs &a, const RouteKeys &rk, int t, const float *lg) {
+// One warp per token (P1b, all blocks): logits = sum of the K parts in part
+// order (lanes own experts lane + 32 i), staged in a warp-private smem row.
+// Expert e is selected iff fewer than k experts beat it, where e' beats e iff
+// l[e'] > l[e] or (l[e'] == l[e] and e' < e) (lowest id wins ties; -0 == +0
+// compare equal).  Its slot is the number of selected experts with a smaller id
+// (slots in ascending expert id, R#4).  Softmax over the k selected:
+// m = max, z_j = expf(l_j - m), Z = ((z_0 + z_1) + ...) in slot order,
+// w_j = z_j / Z (IEEE).
+__device__ void topk_warp(const CallArgs &a, const RouteKeys &rk, int t, float *l) {
   const int lane = threadIdx.x & 31;
   const int E = a.E, k = a.k;
-  uint32_t taken = 0;  // bit i: expert lane + 32 i already selected
-  int sel[kMaxK];
-  float sv[kMaxK];
-  for (int r = 0; r < k; ++r) {
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
-    for (int i = 0; lane + 32 * i < E; ++i) {
-      int e = lane + 32 * i;
-      if (taken & (1u << i)) continue;
-      float v = lg[e];
-      if (v > bv || (v == bv && e < bi)) { bv = v; bi = e; }
-    }
+  const int nkp = router_nkp(a.d, E);
+  const int grp = t / kRouterRows, row = t % kRouterRows;
+  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * E + row * E;
+  const int nw = (E + 31) / 32;  // <= 8 experts per lane
+  float val[8];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  for (int i = 0; i < 8; ++i) {
+    val[i] = 0.f;
+    const int e = lane + 32 * i;
+    if (i < nw && e < E) {
+      float p[8];
+      float s = 0.f;
+      for (int q0 = 0; q0 < nkp; q0 += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          p[u] = (q0 + u < nkp) ? __ldcg(src + (size_t)(q0 + u) * kRouterRows * E + e) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q0 + u < nkp) s = (q0 + u == 0) ? p[u] : s + p[u];
+      }
+      val[i] = s;
+      l[e] = s;
     }
-    sel[r] = bi;
-    sv[r] = bv;
-    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
   }
-  if (lane == 0) {
-    for (int q = 1; q < k; ++q) {
-      int ve = sel[q];
-      float vv = sv[q];
-      int b = q - 1;
-      while (b >= 0 && sel[b] > ve) { sel[b + 1] = sel[b]; sv[b + 1] = sv[b]; --b; }
-      sel[b + 1] = ve;
-      sv[b + 1] = vv;
+  __syncwarp();
+  int slot_of[8];
+  int below = 0;  // selected experts in lower 32-chunks
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    slot_of[i] = -1;
+    if (i < nw) {
+      const int e = lane + 32 * i;
+      bool sel = false;
+      if (e < E) {
+        const float v = val[i];
+        int beat = 0;
+#pragma unroll 8
+        for (int e2 = 0; e2 < E; ++e2) {
+          const float v2 = l[e2];
+          beat += (v2 > v) || (v2 == v && e2 < e);
+        }
+        sel = beat < k;
+      }
+      const unsigned int bal = __ballot_sync(0xffffffffu, sel);
+      if (sel) {
+        slot_of[i] = below + __popc(bal & ((1u << lane) - 1u));
+        m = fmaxf(m, val[i]);
+      }
+      below += __popc(bal);
     }
-    float m = sv[0];
-    for (int j = 1; j < k; ++j) m = fmaxf(m, sv[j]);
-    float z[kMaxK], Z = 0.f;
-    for (int j = 0; j < k; ++j) { z[j] = expf(sv[j] - m); Z = Z + z[j]; }
-    for (int j = 0; j < k; ++j) {
-      const int key = rk.key[sel[j]];
-      a.idx[(size_t)t * k + j] = sel[j];
-      a.w[(size_t)t * k + j] = __fdiv_rn(z[j], Z);
-      a.key[(size_t)t * k + j] = key;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float z[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) z[i] = (slot_of[i] >= 0) ? expf(val[i] - m) : 0.f;
+  float Z = 0.f;
+  for (int j = 0; j < k; ++j) {  // fixed slot order
+    float zj = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const unsigned int b = __ballot_sync(0xffffffffu, slot_of[i] == j);
+      if (b) zj = __shfl_sync(0xffffffffu, z[i], __ffs(b) - 1);
+    }
+    Z = (j == 0) ? zj : Z + zj;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (slot_of[i] >= 0) {
+      const int e = lane + 32 * i, j = slot_of[i];
+      a.idx[(size_t)t * k + j] = e;
+      a.w[(size_t)t * k + j] = __fdiv_rn(z[i], Z);
+      a.key[(size_t)t * k + j] = rk.key[e];
     }
   }
   __syncwarp();
@@ -239,10 +307,16 @@ __device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
   const bool sys = a.world > 1;
   for (int K = tid; K < nkeys; K += blockDim.x) {
     int run = 0;
-    for (int b = 0; b < nchunks; ++b) {
-      int c = __ldcg(a.bcnt + (size_t)b * nkeys + K);
-      a.bcnt[(size_t)b * nkeys + K] = run;  // exclusive chunk base
-      run += c;
+    for (int b0 = 0; b0 < nchunks; b0 += 8) {  // 8 loads in flight
+      int c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] = (b0 + u < nchunks) ? __ldcg(a.bcnt + (size_t)(b0 + u) * nkeys + K) : 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b0 + u < nchunks) {
+          a.bcnt[(size_t)(b0 + u) * nkeys + K] = run;  // exclusive chunk base
+          run += c[u];
+        }
     }
     tot[K] = run;
     a.stats[K] += run;
@@ -295,14 +369,22 @@ __device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
 }
 
 // --------------------------------------------------------------------- P4
-// Warp copy of one row of nch 16-B chunks: all loads of a lane before its stores.
+// Warp copy of one row of nch 16-B chunks: up to 16 loads of a lane in flight
+// before its stores (the copy is latency-bound per warp).
 __device__ __forceinline__ void copy_row(uint4 *__restrict__ dst, const uint4 *__restrict__ src, int nch, int lane) {
-  int c = lane;
-  for (; c + 96 < nch; c += 128) {
-    uint4 v0 = __ldg(src + c), v1 = __ldg(src + c + 32), v2 = __ldg(src + c + 64), v3 = __ldg(src + c + 96);
-    dst[c] = v0; dst[c + 32] = v1; dst[c + 64] = v2; dst[c + 96] = v3;
+  for (int c0 = lane; c0 < nch; c0 += 16 * 32) {
+    uint4 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int c = c0 + 32 * u;
+      if (c < nch) v[u] = __ldg(src + c);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int c = c0 + 32 * u;
+      if (c < nch) dst[c] = v[u];
+    }
   }
-  for (; c < nch; c += 32) dst[c] = __ldg(src + c);
 }
 
 __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallArgs a,
@@ -315,21 +397,46 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
   // ---- P1 router (+ reset of the GEMM counters of this call)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x < 4) a.sync[threadIdx.x] = 0;
+  TG_STAMP(8);
   const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
-  const int nkp = router_kparts(a.d);
-  for (int it = blockIdx.x; it < ngroups * nkp; it += gridDim.x)
-    router_item(a, rk, it / nkp, it % nkp, reinterpret_cast<float *>(fsm));
+  {
+    const int nkp = router_nkp(a.d, a.E), KP = router_kpart(a.d, a.E), Epad = router_epad(a.E);
+    RouterSmem R;
+    R.ldw = KP / 2 + 4;
+    R.wg = reinterpret_cast<uint32_t *>(fsm);
+    R.xt = R.wg + Epad * R.ldw;
+    R.part = reinterpret_cast<float *>(R.xt + kRouterRows * R.ldw);
+    const int bpp = gridDim.x / nkp;  // blocks per K part
+    const int kp = blockIdx.x % nkp, slot = blockIdx.x / nkp;
+    if (slot < bpp && slot < ngroups) {
+      router_stage_wg(a, R, kp);
+      TG_STAMP(9);
+      int it = 0;
+      for (int grp = slot; grp < ngroups; grp += bpp, ++it) {
+        if (it < 5) TG_STAMP(20 + 2 * it);
+        router_item(a, rk, R, grp, kp);
+        if (it < 5) TG_STAMP(21 + 2 * it);
+      }
+    }
+  }
+  if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + blockIdx.x] = globaltimer_ns();
   grid_barrier(gbar, a.epoch, kFrontBars, 0, a.err);
+  // ---- P1b top-k + softmax + ERT key, one warp per token over the whole grid
+  {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    float *lrow = reinterpret_cast<float *>(fsm) + (threadIdx.x >> 5) * a.E;
+    for (int t = gw; t < a.T; t += nw) topk_warp(a, rk, t, lrow);
+  }
+  grid_barrier(gbar, a.epoch, kFrontBars, 1, a.err);
   TG_STAMP(1);
   // ---- P2 rank (+ reset of the router group counters for the next call)
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ngroups; i += gridDim.x * blockDim.x) a.grp_ctr[i] = 0;
   const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
   for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, fsm);
-  grid_barrier(gbar, a.epoch, kFrontBars, 1, a.err);
+  grid_barrier(gbar, a.epoch, kFrontBars, 2, a.err);
   TG_STAMP(2);
   // ---- P3 counts exchange + layout (block 0)
   if (blockIdx.x == 0) exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(fsm));
-  grid_barrier(gbar, a.epoch, kFrontBars, 2, a.err);
+  grid_barrier(gbar, a.epoch, kFrontBars, 3, a.err);
   TG_STAMP(3);
   // the GEMM kernel may launch now: its prologue overlaps the dispatch
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -379,7 +486,9 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
 }
 
 static size_t front_smem(const CallArgs &a) {
-  size_t r = sizeof(float) * std::max(8 * kRouterRows * 64, kRouterRows * a.E);
+  const int KP = router_kpart(a.d, a.E), ldw = KP / 2 + 4;
+  size_t r = sizeof(uint32_t) * (size_t)(router_epad(a.E) + kRouterRows) * ldw +
+             sizeof(float) * std::max(8 * kRouterRows * 64, kRouterRows * (a.E + 1));
   size_t b = sizeof(uint32_t) * 8 * a.nkeys;
   size_t e = sizeof(int32_t) * 3 * a.nkeys;
   return std::max(r, std::max(b, e));
@@ -388,7 +497,7 @@ static size_t front_smem(const CallArgs &a) {
 cudaError_t launch_front(const CallArgs &a, const RouteKeys &rk, int n_sms, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
   }

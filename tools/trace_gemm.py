@@ -43,8 +43,14 @@ def main():
         print("front kernel phase stamps (us from start: router, rank, exchange, dispatch):",
               np.round((st[:5] - st[0]) / 1e3, 2).tolist())
         t0g = tr["start"].min()
+        print("router detail (us from front start): zero-ctr %.2f wg-staged %.2f | item0: start %.2f x-tile %.2f mma+partials %.2f fence %.2f topk-start %.2f topk-end %.2f" % tuple((st[i] - st[0]) / 1e3 if st[i] else -1 for i in (8, 9, 10, 11, 12, 13, 14, 15)))
+        print("block0 items (start,end) us:", [(round((st[20 + 2 * i] - st[0]) / 1e3, 2), round((st[21 + 2 * i] - st[0]) / 1e3, 2)) for i in range(5) if st[20 + 2 * i]])
+        fb = (tr["front_block_p1"] - st[0]) / 1e3
+        print("front P1 finish per block: min %.1f median %.1f max %.1f  argmax %d" % (fb.min(), np.median(fb), fb.max(), int(np.argmax(fb))))
+        tc = tr["topk_cycles"]
+        print("per-block gather/topk kcycles (cumulative over traced calls): max gather %.1f max topk %.1f, block of max topk %d" % (tc[:, 0].max() / 1e3, tc[:, 1].max() / 1e3, int(np.argmax(tc[:, 1]))))
         print("gemm: CTA start %.1f us after front start; grid barrier at %.1f, combine done %.1f us after GEMM start"
-              % ((t0g - st[0]) / 1e3, (st[8] - t0g) / 1e3, (st[9] - t0g) / 1e3))
+              % ((t0g - st[0]) / 1e3, (st[16] - t0g) / 1e3, (st[17] - t0g) / 1e3))
     np.savez(os.path.join(ROOT, "gpurun_out", f"trace_{a.config}_{T}.npz"), **tr)
     analyze(tr)
 
