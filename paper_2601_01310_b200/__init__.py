@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtarragon.so")
+LIB_PATH = os.environ.get("TG_LIB_PATH") or os.path.join(_HERE, "libtarragon.so")  # override: A/B timing only
 
 TG_OK, TG_ERR_INVALID, TG_ERR_NO_ROUTE, TG_ERR_NOT_LOADED = 0, -1, -2, -3
 TG_ERR_STALE_VERSION, TG_ERR_CUDA, TG_ERR_PEER, TG_ERR_OOM, TG_ERR_UNSUPPORTED = -4, -5, -6, -7, -8

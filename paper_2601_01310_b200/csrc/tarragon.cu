@@ -77,6 +77,7 @@ struct tg_ctx {
   int *err_host = nullptr, *err_dev = nullptr;
   uint64_t *trace = nullptr;                     // device trace buffer (diagnostics)
   bool tracing = false;
+  int force_mode = -1;                           // TG_WIDE=0/1 (development A/B), -1 auto
   bf16 *x_stage = nullptr, *out_stage = nullptr;   // for tg_moe_layer_host
   uint32_t epoch = 0;
   int last_T = 0;
@@ -243,9 +244,9 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   // local scratch
   const int nblk_max = (int)((Tm + kRankBlock - 1) / kRankBlock);
   const int ftiles = (F + BM - 1) / BM, ctiles = (d + BM - 1) / BM;
-  const int nt_max = (c->R_cap + BN_MAX - 1) / BN_MAX + (int)S_loc + 1;
+  const int nt_max = (c->R_cap + 127) / 128 + (int)S_loc + 1;  // narrow tiles: the most units
   const int ftiles_sh = Fsh > 0 ? (Fsh + BM - 1) / BM : 0;
-  const int nt_sh = (int)((Tm + BN_MAX - 1) / BN_MAX);
+  const int nt_sh = (int)((Tm + 127) / 128);
   c->args.n_units_max = nt_max * (ftiles + ctiles * c->nsplit) + nt_sh * (ftiles_sh + ctiles) + 16;
   c->args.n_ctr_max = nt_max * (1 + ctiles) + nt_sh + 16;
   size_t so = 0;
@@ -284,6 +285,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   {
     const char *e = getenv("TG_PDL");  // development switch for A/B timing; default on
     a.pdl = (e && e[0] == '0') ? 0 : 1;
+    const char *wm = getenv("TG_WIDE");
+    if (wm && (wm[0] == '0' || wm[0] == '1')) c->force_mode = wm[0] - '0';
   }
   CKI(cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
   *c->err_host = 0;
@@ -478,6 +481,16 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   a.x = reinterpret_cast<const bf16 *>(x);
   a.out = reinterpret_cast<bf16 *>(out);
   a.epoch = ++c->epoch;
+  {
+    // Wide token tiles (bn = 256) cut the L2 bytes per FLOP of prefill tiles but
+    // measured slower on B200 (per-SM L2->SMEM delivery, not bytes/FLOP, limits
+    // them; profiles/README.md r01): narrow by default, wide on request.
+    bool wide = false;
+    if (c->force_mode >= 0) wide = c->force_mode == 1;  // TG_WIDE development override
+    a.bn = wide ? 256 : 128;
+    a.nstages = wide ? 3 : 4;
+    a.stage_bytes = wide ? 65536 : 49152;
+  }
   a.trace = c->tracing ? c->trace : nullptr;
   for (int q = 0; q < kMaxWorld; ++q) a.sym[q] = q < c->world ? c->peer[q] : nullptr;
   c->n_ev = 0;

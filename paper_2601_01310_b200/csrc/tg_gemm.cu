@@ -52,7 +52,9 @@ struct GemmShared {
   int roff[kMaxPlan];      // reduction-group offsets
 };
 
-__device__ __forceinline__ float silu_f(float a) { return __fdiv_rn(a, 1.0f + expf(-a)); }
+// silu(a) = a / (1 + e^-a) with the fast exp/divide (relative error ~1e-7, far
+// below the bf16 rounding of h that follows; the oracle computes it in fp64).
+__device__ __forceinline__ float silu_f(float a) { return __fdividef(a, 1.0f + __expf(-a)); }
 
 __device__ __forceinline__ int box_index(int nrows) { return ((nrows + 15) >> 4) - 1; }
 
@@ -68,7 +70,7 @@ __device__ void build_plan(const CallArgs &a, GemmShared *P) {
   for (int s = s0; s < s1; ++s) {
     const bool sh = (s == S);
     const int rows = sh ? a.T : __ldcg(a.slot_rows + s);
-    const int nt = (rows + BN_MAX - 1) / BN_MAX;
+    const int nt = (rows + a.bn - 1) / a.bn;
     const int ns = sh ? 1 : a.nsplit;
     P->rows[s] = rows;
     P->nt[s] = nt;
@@ -144,8 +146,8 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
     U.kind = sh ? U_G1_SH : U_G1;
     U.slot = sh ? 0 : s;
     U.m0 = f * BM;
-    U.n0 = P->rowoff[s] + n * BN_MAX;
-    U.nrows = min(BN_MAX, P->rows[s] - n * BN_MAX);
+    U.n0 = P->rowoff[s] + n * a.bn;
+    U.nrows = min(a.bn, P->rows[s] - n * a.bn);
     U.kb0 = 0;
     U.kb1 = a.d / BK;
     U.dep = P->goff[s] + n;
@@ -166,8 +168,8 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
     U.kind = sh ? U_G2_SH : U_G2;
     U.slot = sh ? 0 : s;
     U.m0 = c * BM;
-    U.n0 = P->rowoff[s] + n * BN_MAX;
-    U.nrows = min(BN_MAX, P->rows[s] - n * BN_MAX);
+    U.n0 = P->rowoff[s] + n * a.bn;
+    U.nrows = min(a.bn, P->rows[s] - n * a.bn);
     U.kb0 = sp * (kbF / ns);
     U.kb1 = (sp + 1) * (kbF / ns);
     U.dep = P->goff[s] + n;
@@ -185,7 +187,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // 1024-B aligned stage ring (128-B swizzle atoms), bookkeeping after it.
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t *ring = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
-  GemmShared *S = reinterpret_cast<GemmShared *>(ring + kStages * kStageBytes);
+  GemmShared *S = reinterpret_cast<GemmShared *>(ring + kRingBytes);
+  const int nstages = a.nstages, stage_bytes = a.stage_bytes;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int *err = a.err;
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t bbytes = (uint32_t)(bi + 1) * 16 * BK * 2;
         const uint32_t abytes = (g1 ? 2u : 1u) * kTileBytes;
         const uint32_t sub = abytes + bbytes;             // one 64-wide K block of A tile(s) + B tile
-        const int kps = max(1, (int)(kStageBytes / sub));  // K blocks per stage (2 for decode GEMM2)
+        const int kps = max(1, (int)(stage_bytes / sub));  // K blocks per stage (2 for decode GEMM2)
         const CUtensorMap *mA0 = g1 ? (sh ? &maps.w1s : &maps.w1) : (sh ? &maps.w2s : &maps.w2);
         const CUtensorMap *mA1 = sh ? &maps.w3s : &maps.w3;
         const CUtensorMap *mB = g1 ? &maps.x[bi] : (sh ? &maps.hs[bi] : &maps.h[bi]);
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = U.kb0; kb < U.kb1; kb += kps) {
           const int cnt = min(kps, U.kb1 - kb);
           mbar_wait(&S->empty[stage], phase ^ 1, err);
-          uint8_t *st = ring + stage * kStageBytes;
+          uint8_t *st = ring + stage * stage_bytes;
           mbar_arrive_expect_tx(&S->full[stage], (uint32_t)cnt * sub);
           for (int i = 0; i < cnt; ++i) {
             uint8_t *sb = st + i * sub;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (g1) tma_load_2d(sb + kTileBytes, mA1, &S->full[stage], (kb + i) * BK, rowA, pol_w);
             tma_load_2d(sb + abytes, mB, &S->full[stage], (kb + i) * BK, rowB, pol_x);
           }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == nstages) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -279,6 +282,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ===================== MMA issuer =====================
       int stage = 0;
       uint32_t phase = 0;
+      // per-half use counters as scalars: no local-memory arrays on the issuer's critical path
+      int ecnt0 = 0, ecnt1 = 0, next_h = 0;
       for (int it = 0;; ++it) {
         const int r = it % kSchedDepth;
         mbar_wait(&S->sfull[r], (it / kSchedDepth) & 1, err);
@@ -287,21 +292,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (u < 0) break;
         const Unit U = decode_unit(a, S, u);
         const bool g1 = (U.kind == U_G1 || U.kind == U_G1_SH);
-        const int buf = it & 1;
-        mbar_wait(&S->tempty[buf], ((it >> 1) & 1) ^ 1, err);
-        tc_fence_after();
         const int nb = (box_index(U.nrows) + 1) * 16;
+        // TMEM = two 256-column halves; a wide GEMM1 unit (nb > 128) takes both
+        // (a1 in half 0, a3 in half 1), every other unit one half, alternating.
+        const bool wide1 = g1 && nb > 128;
+        int h;
+        if (wide1) {
+          h = 0;
+          mbar_wait(&S->tempty[0], (ecnt0 & 1) ^ 1, err);
+          mbar_wait(&S->tempty[1], (ecnt1 & 1) ^ 1, err);
+          ++ecnt0;
+          ++ecnt1;
+        } else {
+          h = next_h;
+          next_h ^= 1;
+          const int e = h ? ecnt1 : ecnt0;
+          mbar_wait(&S->tempty[h], (e & 1) ^ 1, err);
+          if (h) ++ecnt1; else ++ecnt0;
+        }
+        tc_fence_after();
         const uint32_t idesc = idesc_bf16_f32(BM, nb);
-        const uint32_t d0 = tmem + buf * 256, d1 = tmem + buf * 256 + 128;
+        const uint32_t d0 = tmem + (wide1 ? 0 : h * 256), d1 = wide1 ? tmem + 256 : d0 + 128;
         const uint32_t abytes = (g1 ? 2u : 1u) * kTileBytes;
         const uint32_t sub = abytes + (uint32_t)nb * BK * 2;
-        const int kps = max(1, (int)(kStageBytes / sub));
+        const int kps = max(1, (int)(stage_bytes / sub));
         for (int kb = U.kb0; kb < U.kb1; kb += kps) {
           const int cnt = min(kps, U.kb1 - kb);
           mbar_wait(&S->full[stage], phase, err);
           tc_fence_after();
           for (int i = 0; i < cnt; ++i) {
-            const uint32_t sa = smem_u32(ring + stage * kStageBytes + i * sub);
+            const uint32_t sa = smem_u32(ring + stage * stage_bytes + i * sub);
             const uint64_t dA0 = desc_sw128_kmajor(sa);
             const uint64_t dA1 = desc_sw128_kmajor(sa + kTileBytes);
             const uint64_t dB = desc_sw128_kmajor(sa + abytes);
@@ -314,9 +334,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
           umma_commit(&S->empty[stage]);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == nstages) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&S->tfull[buf]);
+        umma_commit(&S->tfull[h]);
       }
     }
   } else if (warp >= 4) {
@@ -324,6 +344,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;            // TMEM lane quarter of this warp
     const int et = threadIdx.x - 128;  // 0..127
     const int2 *meta = reinterpret_cast<const int2 *>(a.sym[a.rank] + a.L.meta);
+    int fcnt0 = 0, fcnt1 = 0, next_h = 0;
     for (int it = 0;; ++it) {
       const int r = it % kSchedDepth;
       mbar_wait(&S->sfull[r], (it / kSchedDepth) & 1, err);
@@ -334,11 +355,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const Unit U = decode_unit(a, S, u);
       const bool g1 = (U.kind == U_G1 || U.kind == U_G1_SH);
       const bool sh = (U.kind == U_G1_SH || U.kind == U_G2_SH);
-      const int buf = it & 1;
-      mbar_wait(&S->tfull[buf], (it >> 1) & 1, err);
+      const int nb = (box_index(U.nrows) + 1) * 16;
+      const bool wide1 = g1 && nb > 128;
+      int h;
+      if (wide1) h = 0; else { h = next_h; next_h ^= 1; }
+      mbar_wait(&S->tfull[h], (h ? fcnt1 : fcnt0) & 1, err);
+      if (h) ++fcnt1; else ++fcnt0;
       tc_fence_after();
       const int m = U.m0 + q * 32 + lane;  // weight row handled by this thread
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + buf * 256;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (wide1 ? 0 : h * 256);
+      const int a3off = wide1 ? 256 : 128;
       if (g1) {
         const int Fw = sh ? a.Fsh : a.F;
         bf16 *Hout = sh ? a.Hs : a.H;
@@ -346,7 +372,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int c0 = 0; c0 < U.nrows; c0 += 32) {
           uint32_t r1[32], r3[32];
           tmem_ld_32x32b_x32(tbase + c0, r1);
-          tmem_ld_32x32b_x32(tbase + 128 + c0, r3);
+          tmem_ld_32x32b_x32(tbase + a3off + c0, r3);
           tmem_ld_wait();
           if (m < Fw) {
 #pragma unroll
@@ -360,7 +386,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&S->tempty[buf]);
+        mbar_arrive(&S->tempty[h]);
+        if (wide1) mbar_arrive(&S->tempty[1]);
         // publish H rows: generic -> async proxy, then release the group counter
         fence_proxy_async_global();
         named_bar_sync(1, 128);
@@ -394,7 +421,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&S->tempty[buf]);
+        mbar_arrive(&S->tempty[h]);
         if (split) {
           // fixed-order split-K reduction ((p0 + p1) + p2) + ... by the last split to finish
           __threadfence();
@@ -524,7 +551,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) a.trace[a.n_units_max + 148 + 17] = globaltimer_ns();
 }
 
-size_t gemm_smem_bytes() { return 1024 + (size_t)kStages * kStageBytes + sizeof(GemmShared); }
+size_t gemm_smem_bytes() { return 1024 + (size_t)kRingBytes + sizeof(GemmShared); }
 
 cudaError_t gemm_configure() {
   return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes());

@@ -15,17 +15,20 @@ constexpr int kMaxExperts = 256;
 constexpr int kMaxK = 8;
 constexpr int kMaxKeys = 1024;      // world * S_max  (key = rank * S_max + bank slot)
 constexpr int kRankBlock = 256;     // tokens per block of the rank kernel
-constexpr int kNumBoxes = 8;        // token-tile heights 16, 32, ..., 128
+constexpr int kNumBoxes = 16;       // token-tile heights 16, 32, ..., 256
 constexpr int kMaxSlotsPerRank = 256;
 
-// GEMM tiling (see DESIGN.md §6): swap-AB, weights fill UMMA M = 128,
-// tokens are UMMA N (16..128), K staged 64 wide (one 128-B swizzle row).
+// GEMM tiling (see DESIGN.md §2): swap-AB, weights fill UMMA M = 128,
+// tokens are UMMA N (16..bn), K staged 64 wide (one 128-B swizzle row).
+// Two modes per call: narrow (bn = 128, 4 stages x 48 KB: decode) and wide
+// (bn = 256, 3 stages x 64 KB: prefill, halves the L2 bytes per FLOP of the
+// weight tiles).
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int BN_MAX = 128;
-constexpr int kStages = 4;
+constexpr int BN_MAX = 256;
+constexpr int kStages = 4;                      // maximum (narrow mode)
 constexpr int kTileBytes = 16384;               // 128 rows x 128 B
-constexpr int kStageBytes = 3 * kTileBytes;     // A0 (W1|W2), A1 (W3), B (X|H)
+constexpr int kRingBytes = 196608;              // 4 x 48 KB (narrow) or 3 x 64 KB (wide)
 constexpr int kSchedDepth = 8;
 constexpr int kGemmThreads = 256;               // w0 TMA, w1 MMA, w2 TMEM, w4-7 epilogue
 constexpr int kTmemCols = 512;                  // 2 accumulator buffers x 256 columns
@@ -79,6 +82,7 @@ struct CallArgs {
   // shape
   int d, E, k, F, Fsh, world, rank, S_max, S_loc, nkeys, T_max, R_cap, R_sh0, nsplit;
   int T;                 // tokens on this rank for this call
+  int bn, nstages, stage_bytes;  // GEMM token-tile width and stage ring geometry of this call
   uint32_t epoch;
   // inputs / outputs
   const bf16 *x;

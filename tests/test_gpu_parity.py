@@ -127,6 +127,20 @@ def test_ragged_and_multi_tile(T):
     compare(ref, wl.as_u16(out), rt)
 
 
+@pytest.mark.parametrize("cfg,T", [("tiny", 1000), ("qwen_prefill", None)])
+def test_wide_tile_mode_parity(cfg, T, monkeypatch):
+    """GEMM wide token tiles (bn = 256, TMEM halves shared by a1|a3): same parity and mask identity."""
+    monkeypatch.setenv("TG_WIDE", "1")
+    if cfg == "tiny":
+        tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1006, T=T)
+        out = _run(layer, x)
+        compare(oracle_layer(L, x, pl, [0, 0], G=1), wl.as_u16(out), layer.routing(T))
+        layer.mask_worker(1, 1)
+        assert torch.equal(out.view(torch.int16), _run(layer, x).view(torch.int16))
+    else:
+        _big(cfg, 2004, n_sample=16, W=4)
+
+
 def test_empty_call_and_errors():
     tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1004, T=16, T_max=64)
     empty = torch.empty(0, sh.d, dtype=torch.bfloat16, device="cuda")
