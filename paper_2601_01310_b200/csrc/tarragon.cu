@@ -272,6 +272,13 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   a.S_max = c->S_max; a.S_loc = c->S_loc; a.nkeys = c->nkeys; a.T_max = c->T_max; a.R_cap = c->R_cap;
   a.R_sh0 = c->R_sh0; a.nsplit = c->nsplit;
   a.wg = c->wg;
+  a.bank_w1 = c->bank_w1;
+  a.bank_w3 = c->bank_w3;
+  {
+    // L2 prefetch budget: ~40% of L2 for the weights the GEMM streams first
+    const char *e = getenv("TG_L2PF");  // development override (bytes; 0 = off)
+    a.l2_prefetch_bytes = e ? atoll(e) : (long long)(prop.l2CacheSize * 0.4);
+  }
   a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.key = (int32_t *)(sb + o_key);
   a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
   a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);

@@ -155,6 +155,7 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
     U.split = 0;
     U.nsplit = 1;
     U.dep_target = 0;
+    U.ntiles = P->nt[s];
   } else {
     const int u2 = u - P->G1;
     const int s = find_seg(P->g2off, NS, u2);
@@ -177,6 +178,7 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
     U.red = (ns > 1) ? P->goff[NS] + P->roff[s] + c * nt + n : -1;
     U.split = sp;
     U.nsplit = ns;
+    U.ntiles = nt;
   }
   return U;
 }
@@ -222,7 +224,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ===================== TMA producer =====================
-      const uint64_t pol_w = policy_evict_first();   // weights: streamed once
+      const uint64_t pol_w1 = policy_evict_first();  // weight tiles streamed once (one token tile)
+      const uint64_t pol_wn = policy_evict_last();   // weight tiles re-read by several token tiles
       const uint64_t pol_x = policy_evict_last();    // token tiles: re-read by every weight tile
       // Dispatched rows from peers must have landed (release/acquire on
       // per-source epoch flags), then order them before async-proxy reads.
@@ -262,6 +265,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const CUtensorMap *mB = g1 ? &maps.x[bi] : (sh ? &maps.hs[bi] : &maps.h[bi]);
         const int rowA = g1 ? U.slot * (sh ? a.Fsh : a.F) + U.m0 : U.slot * a.d + U.m0;
         const int rowB = (!g1 && sh) ? U.n0 - a.R_sh0 : U.n0;
+        const uint64_t pol_w = (U.ntiles > 1) ? pol_wn : pol_w1;
         for (int kb = U.kb0; kb < U.kb1; kb += kps) {
           const int cnt = min(kps, U.kb1 - kb);
           mbar_wait(&S->empty[stage], phase ^ 1, err);

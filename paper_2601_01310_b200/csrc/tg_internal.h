@@ -55,6 +55,7 @@ struct Unit {
   int32_t split;   // split index
   int32_t nsplit;  // number of splits
   int32_t dep_target;
+  int32_t ntiles;  // token tiles of this slot (> 1: the weight tile is re-read, keep it in L2)
 };
 
 struct TmaMaps {
@@ -88,6 +89,8 @@ struct CallArgs {
   const bf16 *x;
   bf16 *out;
   const bf16 *wg;
+  const bf16 *bank_w1, *bank_w3;  // expert bank (L2 prefetch of the first GEMM1 tiles)
+  long long l2_prefetch_bytes;    // budget of that prefetch (0 = off)
   // per-call scratch (local)
   int32_t *idx;          // [T_max][k]
   float *w;              // [T_max][k]

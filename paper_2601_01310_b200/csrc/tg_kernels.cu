@@ -394,6 +394,26 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
   // PDL: everything below reads/writes state of the previous call's GEMM kernel
   asm volatile("griddepcontrol.wait;" ::: "memory");
   TG_STAMP(0);
+  // ---- L2 prefetch of the weights the GEMM streams first.  The GEMM takes its
+  // GEMM1 units slot by slot; the first slot with rows is predicted from the
+  // previous call's per-slot counts (routing is sticky across decode steps).  A
+  // wrong guess only costs idle HBM bandwidth during this (latency-bound) kernel.
+  if (threadIdx.x == 0 && a.l2_prefetch_bytes > 0) {
+    int s0 = -1;
+    for (int s = 0; s < a.S_loc && s0 < 0; ++s)
+      if (__ldcg(a.slot_rows + s) > 0) s0 = s;
+    if (s0 >= 0) {
+      const long long per_mat = min((long long)a.F * a.d * 2, a.l2_prefetch_bytes / 2);  // W1 and W3 halves
+      const long long chunk = 65536;
+      const long long nch = per_mat / chunk;
+      const uint8_t *b1 = reinterpret_cast<const uint8_t *>(a.bank_w1) + (size_t)s0 * a.F * a.d * 2;
+      const uint8_t *b3 = reinterpret_cast<const uint8_t *>(a.bank_w3) + (size_t)s0 * a.F * a.d * 2;
+      for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
+        prefetch_l2_bulk(b1 + c * chunk, (uint32_t)chunk);
+        prefetch_l2_bulk(b3 + c * chunk, (uint32_t)chunk);
+      }
+    }
+  }
   // ---- P1 router (+ reset of the GEMM counters of this call)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x < 4) a.sync[threadIdx.x] = 0;
