@@ -78,6 +78,7 @@ struct tg_ctx {
   uint64_t *trace = nullptr;                     // device trace buffer (diagnostics)
   bool tracing = false;
   int force_mode = -1;                           // TG_WIDE=0/1 (development A/B), -1 auto
+  int force_dual = -1;                           // TG_G2DUAL=0/1 (development A/B), -1 auto
   bf16 *x_stage = nullptr, *out_stage = nullptr;   // for tg_moe_layer_host
   uint32_t epoch = 0;
   int last_T = 0;
@@ -294,6 +295,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
     a.pdl = (e && e[0] == '0') ? 0 : 1;
     const char *wm = getenv("TG_WIDE");
     if (wm && (wm[0] == '0' || wm[0] == '1')) c->force_mode = wm[0] - '0';
+    const char *dm = getenv("TG_G2DUAL");
+    if (dm && (dm[0] == '0' || dm[0] == '1')) c->force_dual = dm[0] - '0';
   }
   CKI(cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
   *c->err_host = 0;
@@ -495,6 +498,9 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
     bool wide = false;
     if (c->force_mode >= 0) wide = c->force_mode == 1;  // TG_WIDE development override
     a.bn = wide ? 256 : 128;
+    // prefill-sized calls (>= 192 rows per expert on average): GEMM2 units take two W2 tiles
+    const long long rows_avg = (long long)T * c->world * c->k / c->E;
+    a.g2dual = !wide && ((rows_avg >= 192 && c->force_dual != 0) || c->force_dual == 1);
     a.nstages = wide ? 3 : 4;
     a.stage_bytes = wide ? 65536 : 49152;
   }

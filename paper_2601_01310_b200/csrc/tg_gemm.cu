@@ -62,7 +62,7 @@ __device__ __forceinline__ int box_index(int nrows) { return ((nrows + 15) >> 4)
 __device__ void build_plan(const CallArgs &a, GemmShared *P) {
   const int lane = threadIdx.x & 31;
   const int S = a.S_loc, nsh = a.Fsh > 0 ? 1 : 0, NS = S + nsh;
-  const int ftiles = (a.F + BM - 1) / BM, ctiles = (a.d + BM - 1) / BM;
+  const int ftiles = (a.F + BM - 1) / BM, ctiles = (a.d + BM * (a.g2dual ? 2 : 1) - 1) / (BM * (a.g2dual ? 2 : 1));
   const int ftiles_sh = nsh ? (a.Fsh + BM - 1) / BM : 0;
   const int per = (NS + 31) / 32;
   const int s0 = min(NS, lane * per), s1 = min(NS, s0 + per);
@@ -156,6 +156,7 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
     U.nsplit = 1;
     U.dep_target = 0;
     U.ntiles = P->nt[s];
+    U.dual = 0;
   } else {
     const int u2 = u - P->G1;
     const int s = find_seg(P->g2off, NS, u2);
@@ -168,7 +169,8 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
     const int kbF = (sh ? a.Fsh : a.F) / BK;
     U.kind = sh ? U_G2_SH : U_G2;
     U.slot = sh ? 0 : s;
-    U.m0 = c * BM;
+    U.m0 = c * BM * (a.g2dual ? 2 : 1);
+    U.dual = a.g2dual;
     U.n0 = P->rowoff[s] + n * a.bn;
     U.nrows = min(a.bn, P->rows[s] - n * a.bn);
     U.kb0 = sp * (kbF / ns);
@@ -257,7 +259,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         const int bi = box_index(U.nrows);
         const uint32_t bbytes = (uint32_t)(bi + 1) * 16 * BK * 2;
-        const uint32_t abytes = (g1 ? 2u : 1u) * kTileBytes;
+        const bool two = g1 || U.dual;                     // two A tiles per K block (W1|W3, or W2 rows m0 and m0+128)
+        const uint32_t abytes = (two ? 2u : 1u) * kTileBytes;
         const uint32_t sub = abytes + bbytes;             // one 64-wide K block of A tile(s) + B tile
         const int kps = max(1, (int)(stage_bytes / sub));  // K blocks per stage (2 for decode GEMM2)
         const CUtensorMap *mA0 = g1 ? (sh ? &maps.w1s : &maps.w1) : (sh ? &maps.w2s : &maps.w2);
@@ -275,6 +278,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint8_t *sb = st + i * sub;
             tma_load_2d(sb, mA0, &S->full[stage], (kb + i) * BK, rowA, pol_w);
             if (g1) tma_load_2d(sb + kTileBytes, mA1, &S->full[stage], (kb + i) * BK, rowA, pol_w);
+            else if (U.dual) tma_load_2d(sb + kTileBytes, mA0, &S->full[stage], (kb + i) * BK, rowA + BM, pol_w);
             tma_load_2d(sb + abytes, mB, &S->full[stage], (kb + i) * BK, rowB, pol_x);
           }
           if (++stage == nstages) { stage = 0; phase ^= 1; }
@@ -317,7 +321,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         const uint32_t idesc = idesc_bf16_f32(BM, nb);
         const uint32_t d0 = tmem + (wide1 ? 0 : h * 256), d1 = wide1 ? tmem + 256 : d0 + 128;
-        const uint32_t abytes = (g1 ? 2u : 1u) * kTileBytes;
+        const bool two = g1 || U.dual;
+        const uint32_t abytes = (two ? 2u : 1u) * kTileBytes;
         const uint32_t sub = abytes + (uint32_t)nb * BK * 2;
         const int kps = max(1, (int)(stage_bytes / sub));
         for (int kb = U.kb0; kb < U.kb1; kb += kps) {
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               const uint32_t acc = (kb > U.kb0 || i > 0 || kk > 0) ? 1u : 0u;
               // advance 16 K-elements = 32 B inside the swizzle row (>>4 units)
               umma_bf16_ss(d0, dA0 + 2 * kk, dB + 2 * kk, idesc, acc);
-              if (g1) umma_bf16_ss(d1, dA1 + 2 * kk, dB + 2 * kk, idesc, acc);
+              if (two) umma_bf16_ss(d1, dA1 + 2 * kk, dB + 2 * kk, idesc, acc);
             }
           }
           umma_commit(&S->empty[stage]);
@@ -401,24 +406,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       } else {
         const bool split = (U.nsplit > 1);
-        for (int c0 = 0; c0 < U.nrows; c0 += 32) {
-          uint32_t r1[32];
-          tmem_ld_32x32b_x32(tbase + c0, r1);
-          tmem_ld_wait();
-          if (m < a.d) {
+        for (int hh = 0; hh < (U.dual ? 2 : 1); ++hh) {  // dual: second W2 tile at +128 rows / columns
+          const int mm = m + hh * BM;
+          for (int c0 = 0; c0 < U.nrows; c0 += 32) {
+            uint32_t r1[32];
+            tmem_ld_32x32b_x32(tbase + hh * 128 + c0, r1);
+            tmem_ld_wait();
+            if (mm < a.d) {
 #pragma unroll
-            for (int n = 0; n < 32; ++n) {
-              if (c0 + n < U.nrows) {
-                const int row = U.n0 + c0 + n;
-                const float v = __uint_as_float(r1[n]);
-                if (split) {
-                  a.ws[((size_t)U.split * a.R_cap + row) * a.d + m] = v;
-                } else if (sh) {
-                  a.ysh[(size_t)(row - a.R_sh0) * a.d + m] = __float2bfloat16_rn(v);
-                } else {
-                  const int2 o = meta[row];
-                  bf16 *yb = reinterpret_cast<bf16 *>(a.sym[o.x] + a.L.ybuf);
-                  yb[(size_t)o.y * a.d + m] = __float2bfloat16_rn(v);
+              for (int n = 0; n < 32; ++n) {
+                if (c0 + n < U.nrows) {
+                  const int row = U.n0 + c0 + n;
+                  const float v = __uint_as_float(r1[n]);
+                  if (split) {
+                    a.ws[((size_t)U.split * a.R_cap + row) * a.d + mm] = v;
+                  } else if (sh) {
+                    a.ysh[(size_t)(row - a.R_sh0) * a.d + mm] = __float2bfloat16_rn(v);
+                  } else {
+                    const int2 o = meta[row];
+                    bf16 *yb = reinterpret_cast<bf16 *>(a.sym[o.x] + a.L.ybuf);
+                    yb[(size_t)o.y * a.d + mm] = __float2bfloat16_rn(v);
+                  }
                 }
               }
             }
@@ -436,8 +444,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __threadfence();
             // 128 threads: 4 row groups x 32 threads x 4 consecutive columns (16-B loads);
             // y[row][c] = bf16(((p0 + p1) + p2) + ...), 8-B bf16 stores to the source AW.
-            const int cg = (et & 31) * 4, rg = et >> 5;
-            const int c = U.m0 + cg;
+            const int rg = et >> 5;
+            for (int cgi = (et & 31) * 4; cgi < BM * (U.dual ? 2 : 1); cgi += 128) {
+            const int c = U.m0 + cgi;
             if (c < a.d) {
               for (int n0 = rg; n0 < U.nrows; n0 += 16) {
                 float4 acc[4];
@@ -480,6 +489,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   }
                 }
               }
+            }
             }
           }
           named_bar_sync(1, 128);

@@ -56,6 +56,7 @@ struct Unit {
   int32_t nsplit;  // number of splits
   int32_t dep_target;
   int32_t ntiles;  // token tiles of this slot (> 1: the weight tile is re-read, keep it in L2)
+  int32_t dual;    // GEMM2: second W2 tile at rows m0 + 128 (accumulator at +128 columns)
 };
 
 struct TmaMaps {
@@ -84,6 +85,7 @@ struct CallArgs {
   int d, E, k, F, Fsh, world, rank, S_max, S_loc, nkeys, T_max, R_cap, R_sh0, nsplit;
   int T;                 // tokens on this rank for this call
   int bn, nstages, stage_bytes;  // GEMM token-tile width and stage ring geometry of this call
+  int g2dual;            // GEMM2 units cover two 128-row W2 tiles sharing one H tile (prefill-sized calls)
   uint32_t epoch;
   // inputs / outputs
   const bf16 *x;

@@ -127,10 +127,12 @@ def test_ragged_and_multi_tile(T):
     compare(ref, wl.as_u16(out), rt)
 
 
-@pytest.mark.parametrize("cfg,T", [("tiny", 1000), ("qwen_prefill", None)])
-def test_wide_tile_mode_parity(cfg, T, monkeypatch):
-    """GEMM wide token tiles (bn = 256, TMEM halves shared by a1|a3): same parity and mask identity."""
-    monkeypatch.setenv("TG_WIDE", "1")
+@pytest.mark.parametrize("mode", ["TG_WIDE", "TG_G2DUAL"])
+@pytest.mark.parametrize("cfg,T", [("tiny", 1000), ("qwen_prefill", None), ("mixtral_decode", None)])
+def test_tile_modes_parity(cfg, T, mode, monkeypatch):
+    """GEMM tile variants forced on: wide token tiles (bn = 256, TMEM halves shared by a1|a3) and dual
+    GEMM2 tiles (two W2 tiles per unit): same parity and mask bit-identity."""
+    monkeypatch.setenv(mode, "1")
     if cfg == "tiny":
         tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1006, T=T)
         out = _run(layer, x)
@@ -138,7 +140,7 @@ def test_wide_tile_mode_parity(cfg, T, monkeypatch):
         layer.mask_worker(1, 1)
         assert torch.equal(out.view(torch.int16), _run(layer, x).view(torch.int16))
     else:
-        _big(cfg, 2004, n_sample=16, W=4)
+        _big(cfg, 2004, n_sample=16, W=4 if cfg == "qwen_prefill" else 2)
 
 
 def test_empty_call_and_errors():
