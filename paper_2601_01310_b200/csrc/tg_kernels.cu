@@ -24,7 +24,6 @@
 
 namespace tg {
 
-constexpr int kFrontBars = 4;  // grid barriers per front call
 
 #define TG_STAMP(i)                                                                     \
   do {                                                                                  \
@@ -322,6 +321,29 @@ __device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
     a.stats[K] += run;
   }
   __syncthreads();
+  if (a.world == 1) {
+    // no peers: the gathered counts are this rank's own
+    for (int K = tid; K < nkeys; K += blockDim.x) {
+      gsum[K] = tot[K];
+      below[K] = 0;
+      a.gcounts[K] = tot[K];
+    }
+    __syncthreads();
+    for (int K = tid; K < nkeys; K += blockDim.x) {
+      const int s = K % a.S_max;
+      int off = 0;
+      for (int s2 = 0; s2 < s; ++s2) off += gsum[s2];
+      a.dbase[K] = off;
+    }
+    if (tid == 0) {
+      int any = 0;
+      for (int K = 0; K < nkeys; ++K) any |= tot[K];
+      a.need_src[0] = any > 0;
+      a.sent_to[0] = any > 0;
+    }
+    for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[s];
+    return;
+  }
   // all-gather: my totals -> cnt_all[par][rank][*] on every peer, then release flags
   for (int q = 0; q < a.world; ++q) {
     int32_t *dst = reinterpret_cast<int32_t *>(a.sym[q] + a.L.cnt_all) + ((size_t)par * a.world + a.rank) * nkeys;
@@ -390,9 +412,14 @@ __device__ __forceinline__ void copy_row(uint4 *__restrict__ dst, const uint4 *_
 __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallArgs a,
                                                   const __grid_constant__ RouteKeys rk) {
   extern __shared__ __align__(16) uint8_t fsm[];
-  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8);
+  // grid barriers of this call count on sync[8 + 4 * (epoch & 1)] (u64) from 0; the other
+  // counter is reset here for the next call (the previous call has completed: PDL wait below)
+  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
   // PDL: everything below reads/writes state of the previous call's GEMM kernel
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
+  int nbar = 0;
   TG_STAMP(0);
   // ---- L2 prefetch of the weights the GEMM streams first.  The GEMM takes its
   // GEMM1 units slot by slot; the first slot with rows is predicted from the
@@ -440,23 +467,27 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
     }
   }
   if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + blockIdx.x] = globaltimer_ns();
-  grid_barrier(gbar, a.epoch, kFrontBars, 0, a.err);
+  grid_barrier_z(gbar, nbar++, a.err);
   // ---- P1b top-k + softmax + ERT key, one warp per token over the whole grid
   {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     float *lrow = reinterpret_cast<float *>(fsm) + (threadIdx.x >> 5) * a.E;
     for (int t = gw; t < a.T; t += nw) topk_warp(a, rk, t, lrow);
   }
-  grid_barrier(gbar, a.epoch, kFrontBars, 1, a.err);
+  grid_barrier_z(gbar, nbar++, a.err);
   TG_STAMP(1);
-  // ---- P2 rank (+ reset of the router group counters for the next call)
+  // ---- P2 rank (one chunk of 256 tokens per block)
   const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
   for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, fsm);
-  grid_barrier(gbar, a.epoch, kFrontBars, 2, a.err);
+  // with a single chunk block 0 owns all ranks: P3 follows without a grid barrier
+  if (nchunks > 1) grid_barrier_z(gbar, nbar++, a.err);
   TG_STAMP(2);
   // ---- P3 counts exchange + layout (block 0)
-  if (blockIdx.x == 0) exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(fsm));
-  grid_barrier(gbar, a.epoch, kFrontBars, 3, a.err);
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(fsm));
+  }
+  grid_barrier_z(gbar, nbar++, a.err);
   TG_STAMP(3);
   // the GEMM kernel may launch now: its prologue overlaps the dispatch
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -242,6 +242,24 @@ __device__ __forceinline__ void grid_barrier(unsigned long long *count, uint32_t
   __syncthreads();
 }
 
+// Grid barrier on a counter that starts at 0 for this call (barrier i completes
+// at (i + 1) * gridDim.x arrivals): the number of barriers may vary per call.
+__device__ __forceinline__ void grid_barrier_z(unsigned long long *count, int i, int *err) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long target = (unsigned long long)(i + 1) * gridDim.x;
+    __threadfence();
+    atomicAdd(count, 1ull);
+    if (ld_acquire_gpu_u64(count) < target) {
+      uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_gpu_u64(count) < target)
+        if (globaltimer_ns() - t0 > kWaitTimeoutNs) device_fail(err, 0x3002);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
