@@ -122,6 +122,8 @@ def make_weights_device(shape, seed, device, experts):
         L.shared = (wl.bf16_normal((Fs, d), d ** -0.5, seed * 1000 + 2, device),
                     wl.bf16_normal((Fs, d), d ** -0.5, seed * 1000 + 3, device),
                     wl.bf16_normal((d, Fs), Fs ** -0.5, seed * 1000 + 4, device))
+    if shape.shared_gate:
+        L.wsg = wl.bf16_normal((d,), d ** -0.5, seed * 1000 + 5, device)
     return L
 
 
@@ -145,8 +147,10 @@ def cpu_oracle_sample(shape, L_host, x_host, pl, n_tokens, n_threads):
     sh = tuple(wl.as_u16(a) for a in L_host.shared) if L_host.shared is not None else None
     xs = wl.as_u16(x_host[:n_tokens])
     t0 = time.perf_counter()
+    wsg = wl.as_u16(L_host.wsg) if L_host.wsg is not None else None
     r = oracle.layer(xs, wl.as_u16(L_host.wg), shape.k, w1, w3, w2, pl.cand, pl.ew_rank, pl.slots_per_ew,
-                     np.zeros(pl.n_ews, np.uint8), 1, shared=sh, n_threads=n_threads)
+                     np.zeros(pl.n_ews, np.uint8), 1, shared=sh, n_threads=n_threads,
+                     gate_mode=shape.gate_mode, wsg=wsg)
     dt = time.perf_counter() - t0
     assert r["rc"] == 0
     return n_tokens / dt, dt
@@ -318,7 +322,8 @@ def main():
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         n = args.cpu_sample or 16
         Lh = wl.Layer(shape, L.wg.cpu(), [w.cpu() for w in L.w1], [w.cpu() for w in L.w3],
-                      [w.cpu() for w in L.w2], tuple(w.cpu() for w in L.shared) if L.shared else None)
+                      [w.cpu() for w in L.w2], tuple(w.cpu() for w in L.shared) if L.shared else None,
+                      L.wsg.cpu() if L.wsg is not None else None)
         v, dt = cpu_oracle_sample(shape, Lh, xs[0].cpu(), pl, n, cores)
         cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                "sample": f"first {n} tokens of one batch through O1-O8 (fp64, {cores} threads over tokens), "

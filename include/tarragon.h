@@ -73,6 +73,14 @@ typedef struct {
   const int32_t *ew_rank; /* [n_ews] */
   int slots_per_ew;
   int max_tokens_per_rank;
+  /* Gating variant (R#2 / R#17, SURVEY NEXT-3b):
+   *   gate_mode 0: w = softmax over the k selected logits (renormalised top-k; default);
+   *   gate_mode 1: w = softmax over all E logits, the k selected kept un-renormalised
+   *                (the public DS-V2-Lite / Qwen1.5-MoE routers, norm_topk_prob = false).
+   *   shared_gate 1: the shared expert's output is scaled by sigmoid(x . wsg) per token
+   *                (Qwen1.5-MoE shared_expert_gate; load wsg with tg_load_shared_gate). */
+  int gate_mode;
+  int shared_gate;
 } tg_config;
 
 /* Create a ctx on `cuda_device` (-1: host-only ctx for table/mask logic).
@@ -105,6 +113,9 @@ tg_status tg_load_experts(tg_ctx *ctx, int ew, int slot, int expert_id, const vo
  * Replicated on every rank; added to the routed sum with weight 1.        */
 tg_status tg_load_shared(tg_ctx *ctx, const void *w1, const void *w3, const void *w2,
                          int src_on_device);
+
+/* Shared-expert gate vector wsg [d] bf16 (config shared_gate = 1).  SPMD.   */
+tg_status tg_load_shared_gate(tg_ctx *ctx, const void *wsg, int src_on_device);
 
 /* Expert Routing Table (§4.2): cand[e][c] = (ew, slot) for
  * c < max_cands, primaries then shadows, (-1, -1) padding.  Accepted only

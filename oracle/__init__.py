@@ -53,6 +53,11 @@ def lib():
         L.orc_permute.restype = i32
         L.orc_moe_tokens.argtypes = [i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, i32, P, P, i32]
         L.orc_moe_tokens.restype = i32
+        L.orc_select_mode.argtypes = [P, i32, i32, i32, i32, P, P, P]
+        L.orc_select_mode.restype = i32
+        L.orc_shared_gate.argtypes = [P, P, i32, i32, P]
+        L.orc_moe_tokens2.argtypes = [i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, i32, P, P, i32, P]
+        L.orc_moe_tokens2.restype = i32
         _lib = L
     return _lib
 
@@ -93,14 +98,15 @@ def router(x: np.ndarray, wg: np.ndarray) -> np.ndarray:
     return out
 
 
-def select(logits: np.ndarray, k: int):
-    """O2/O3: (idx int32 [T,k] ascending id, w fp32 [T,k], gap fp32 [T])."""
+def select(logits: np.ndarray, k: int, gate_mode: int = 0):
+    """O2/O3 (gate_mode 0) or O2/O3' (gate_mode 1: softmax over all E, no renormalisation):
+    (idx int32 [T,k] ascending id, w fp32 [T,k], gap fp32 [T])."""
     logits = np.ascontiguousarray(logits, dtype=np.float32)
     T, E = logits.shape
     idx = np.empty((T, k), np.int32)
     w = np.empty((T, k), np.float32)
     gap = np.empty((T,), np.float32)
-    rc = lib().orc_select(_p(logits), T, E, k, _p(idx), _p(w), _p(gap))
+    rc = lib().orc_select_mode(_p(logits), T, E, k, int(gate_mode), _p(idx), _p(w), _p(gap))
     if rc != OK:
         raise ValueError(f"orc_select rc={rc}")
     return idx, w, gap
@@ -113,6 +119,7 @@ def resolve(cand: np.ndarray, ew_rank, ew_slot_base, mask):
     ew_rank = np.ascontiguousarray(ew_rank, dtype=np.int32)
     ew_slot_base = np.ascontiguousarray(ew_slot_base, dtype=np.int32)
     mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    assert mask.size == ew_rank.size, "mask needs one entry per EW"
     rank_e = np.empty(E, np.int32)
     bank_e = np.empty(E, np.int32)
     rc = lib().orc_resolve(E, C, _p(cand), _p(ew_rank), _p(ew_slot_base), _p(mask), _p(rank_e), _p(bank_e))
@@ -135,12 +142,22 @@ def permute(idx: np.ndarray, rank_e, bank_e, G: int, S_max: int):
     return dr, ds, dp, counts
 
 
-def moe_tokens(x, idx, w, w1, w3, w2, shared=None, tokens=None, want_y=False, n_threads=1):
+def shared_gate(x, wsg) -> np.ndarray:
+    """O7': per-token sigmoid weight of the shared expert, fp32 [T]."""
+    x = _u16(x)
+    wsg = _u16(np.ascontiguousarray(wsg).reshape(-1))
+    T, d = x.shape
+    out = np.empty(T, np.float32)
+    lib().orc_shared_gate(_p(x), _p(wsg), T, d, _p(out))
+    return out
+
+
+def moe_tokens(x, idx, w, w1, w3, w2, shared=None, tokens=None, want_y=False, n_threads=1, sgate=None):
     """O6-O8 for the given tokens (all if None).
 
     w1/w3/w2: sequences of E bf16 arrays (W1, W3: [F, d]; W2: [d, F]).
     shared: optional (W1s, W3s, W2s) of the merged shared expert.
-    Returns out bf16 [n, d] (uint16) and, if want_y, y bf16 [n, k, d].
+    Returns out bf16 [n, d] (uint16) and, if want_y, (y bf16 [n, k, d], y_sh bf16 [n, d] or None).
     """
     x = _u16(x)
     T, d = x.shape
@@ -171,14 +188,18 @@ def moe_tokens(x, idx, w, w1, w3, w2, shared=None, tokens=None, want_y=False, n_
         n = tok.size
     out = np.empty((n, d), np.uint16)
     y = np.empty((n, k, d), np.uint16) if want_y else None
-    rc = lib().orc_moe_tokens(d, E, k, F, F_sh, _p(x), _p(idx), _p(w),
-                              ctypes.cast(p1, ctypes.c_void_p), ctypes.cast(p3, ctypes.c_void_p),
-                              ctypes.cast(p2, ctypes.c_void_p), ps[0], ps[1], ps[2],
-                              _p(tok) if tok is not None else None, n, _p(out),
-                              _p(y) if y is not None else None, int(n_threads))
+    ysh = np.empty((n, d), np.uint16) if (want_y and shared is not None) else None
+    sg = None if sgate is None else np.ascontiguousarray(sgate, dtype=np.float32)
+    rc = lib().orc_moe_tokens2(d, E, k, F, F_sh, _p(x), _p(idx), _p(w),
+                               ctypes.cast(p1, ctypes.c_void_p), ctypes.cast(p3, ctypes.c_void_p),
+                               ctypes.cast(p2, ctypes.c_void_p), ps[0], ps[1], ps[2],
+                               _p(sg) if sg is not None else None,
+                               _p(tok) if tok is not None else None, n, _p(out),
+                               _p(y) if y is not None else None, int(n_threads),
+                               _p(ysh) if ysh is not None else None)
     if rc != OK:
         raise ValueError(f"orc_moe_tokens rc={rc}")
-    return (out, y) if want_y else out
+    return (out, (y, ysh)) if want_y else out
 
 
 def slot_bases(n_ews: int, ew_rank, slots_per_ew: int):
@@ -194,14 +215,14 @@ def slot_bases(n_ews: int, ew_rank, slots_per_ew: int):
 
 
 def layer(x, wg, k, w1, w3, w2, cand, ew_rank, slots_per_ew, mask, G, shared=None,
-          tokens=None, n_threads=1, want_y=False):
+          tokens=None, n_threads=1, want_y=False, gate_mode=0, wsg=None):
     """The whole path O1..O8 for global tokens ``x`` (contiguous split over G ranks).
 
     Returns a dict with logits, idx, w, gap, rank_e, bank_e, dst_rank,
     dst_slot, dst_pos, counts, out (for ``tokens`` or all tokens), rc.
     """
     logits = router(x, wg)
-    idx, w, gap = select(logits, k)
+    idx, w, gap = select(logits, k, gate_mode)
     n_ews = len(ew_rank)
     base, S_max = slot_bases(n_ews, ew_rank, slots_per_ew)
     rank_e, bank_e, rc = resolve(cand, ew_rank, base, mask)
@@ -213,9 +234,12 @@ def layer(x, wg, k, w1, w3, w2, cand, ew_rank, slots_per_ew, mask, G, shared=Non
         return res
     dr, ds, dp, counts = permute(idx, rank_e, bank_e, G, S_max)
     res.update(dst_rank=dr, dst_slot=ds, dst_pos=dp, counts=counts)
-    r = moe_tokens(x, idx, w, w1, w3, w2, shared=shared, tokens=tokens, n_threads=n_threads, want_y=want_y)
+    sgate = shared_gate(x, wsg) if (wsg is not None and shared is not None) else None
+    res["sgate"] = sgate
+    r = moe_tokens(x, idx, w, w1, w3, w2, shared=shared, tokens=tokens, n_threads=n_threads, want_y=want_y,
+                   sgate=sgate)
     if want_y:
-        res["out"], res["y"] = r
+        res["out"], (res["y"], res["ysh"]) = r
     else:
         res["out"] = r
     res["rc"] = OK

@@ -127,8 +127,19 @@ void orc_router(const uint16_t *x, const uint16_t *wg, int T, int d, int E, floa
  *     computed in fp64 from the fp32 logits and rounded once to fp32
  *     (R#1/R#2: softmax over the k selected logits = renormalised top-k).
  * Returns ORC_OK. */
+/* O3' (gate_mode 1, NEXT-3b: the public DS-V2-Lite / Qwen1.5-MoE routers,
+ *     norm_topk_prob = false; R#2 variant): softmax over ALL E
+ *     logits, the k selected weights are NOT renormalised:
+ *     w_j = exp(l_j − M) / sum_{e<E} exp(l_e − M), M = max over all E, fp64.
+ *     Selection (O2) is unchanged. */
+int orc_select_mode(const float *logits, int T, int E, int k, int mode, int32_t *idx, float *w, float *gap);
+
 int orc_select(const float *logits, int T, int E, int k, int32_t *idx, float *w, float *gap) {
-    if (k < 1 || k > E || k > ORC_MAX_K) return ORC_ERR_INVALID;
+    return orc_select_mode(logits, T, E, k, 0, idx, w, gap);
+}
+
+int orc_select_mode(const float *logits, int T, int E, int k, int mode, int32_t *idx, float *w, float *gap) {
+    if (k < 1 || k > E || k > ORC_MAX_K || mode < 0 || mode > 1) return ORC_ERR_INVALID;
     int *order = (int *)malloc(sizeof(int) * E);
     int *sel = (int *)malloc(sizeof(int) * k);
     for (int t = 0; t < T; ++t) {
@@ -158,6 +169,10 @@ int orc_select(const float *logits, int T, int E, int k, int32_t *idx, float *w,
         double z[ORC_MAX_K];
         double Z = 0.0;
         for (int j = 0; j < k; ++j) { z[j] = exp((double)l[sel[j]] - m); Z += z[j]; }
+        if (mode == 1) {  /* full softmax denominator; the max over all E is the max selected */
+            Z = 0.0;
+            for (int e = 0; e < E; ++e) Z += exp((double)l[e] - m);
+        }
         for (int j = 0; j < k; ++j) {
             idx[(int64_t)t * k + j] = sel[j];
             w[(int64_t)t * k + j] = (float)(z[j] / Z);
@@ -277,12 +292,44 @@ static void orc_ffn(const uint16_t *x, int d, int F, const uint16_t *W1, const u
  * w1/w3/w2: arrays of E pointers to the per-expert matrices.
  * y_out (optional): [n_tokens][k][d] bf16 per-pair expert outputs.
  * n_threads > 1 parallelises over tokens only (arithmetic per token unchanged). */
+/* O7' shared-expert gate (NEXT-3b: Qwen1.5-MoE shared_expert_gate, DESIGN.md
+ *     R#17 variant): g_t = fp32( sum_i x[t][i] wsg[i] ) accumulated in fp64,
+ *     s_t = fp32( 1 / (1 + exp(-g_t)) ) in fp64; the shared expert's output is
+ *     added with weight s_t instead of 1. */
+void orc_shared_gate(const uint16_t *x, const uint16_t *wsg, int T, int d, float *s_out) {
+    for (int t = 0; t < T; ++t) {
+        double acc = 0.0;
+        for (int i = 0; i < d; ++i) acc += orc_bf16_to_f64(x[(int64_t)t * d + i]) * orc_bf16_to_f64(wsg[i]);
+        float g = (float)acc;
+        s_out[t] = (float)(1.0 / (1.0 + exp(-(double)g)));
+    }
+}
+
+int orc_moe_tokens2(int d, int E, int k, int F, int F_sh,
+                    const uint16_t *x, const int32_t *idx, const float *w,
+                    const uint16_t *const *w1, const uint16_t *const *w3, const uint16_t *const *w2,
+                    const uint16_t *w1s, const uint16_t *w3s, const uint16_t *w2s, const float *sgate,
+                    const int32_t *tokens, int n_tokens, uint16_t *out, uint16_t *y_out,
+                    int n_threads, uint16_t *ysh_out);
+
 int orc_moe_tokens(int d, int E, int k, int F, int F_sh,
                    const uint16_t *x, const int32_t *idx, const float *w,
                    const uint16_t *const *w1, const uint16_t *const *w3, const uint16_t *const *w2,
                    const uint16_t *w1s, const uint16_t *w3s, const uint16_t *w2s,
                    const int32_t *tokens, int n_tokens, uint16_t *out, uint16_t *y_out,
                    int n_threads) {
+    return orc_moe_tokens2(d, E, k, F, F_sh, x, idx, w, w1, w3, w2, w1s, w3s, w2s, NULL, tokens, n_tokens,
+                           out, y_out, n_threads, NULL);
+}
+
+/* sgate (optional, [T] fp32): weight of the shared expert per token (O7'); NULL = 1.
+ * ysh_out (optional, [n_tokens][d] bf16): the shared expert's output y_sh. */
+int orc_moe_tokens2(int d, int E, int k, int F, int F_sh,
+                    const uint16_t *x, const int32_t *idx, const float *w,
+                    const uint16_t *const *w1, const uint16_t *const *w3, const uint16_t *const *w2,
+                    const uint16_t *w1s, const uint16_t *w3s, const uint16_t *w2s, const float *sgate,
+                    const int32_t *tokens, int n_tokens, uint16_t *out, uint16_t *y_out,
+                    int n_threads, uint16_t *ysh_out) {
     if (k < 1 || k > E || d < 1 || F < 1) return ORC_ERR_INVALID;
     int Fmax = F > F_sh ? F : F_sh;
     int bad = 0;
@@ -301,12 +348,16 @@ int orc_moe_tokens(int d, int E, int k, int F, int F_sh,
             orc_ffn(xt, d, F, w1[e], w3[e], w2[e], hbuf, y + (int64_t)j * d);
             if (y_out) memcpy(y_out + ((int64_t)n * k + j) * d, y + (int64_t)j * d, sizeof(uint16_t) * d);
         }
-        if (F_sh > 0) orc_ffn(xt, d, F_sh, w1s, w3s, w2s, hbuf, y + (int64_t)k * d);
+        if (F_sh > 0) {
+            orc_ffn(xt, d, F_sh, w1s, w3s, w2s, hbuf, y + (int64_t)k * d);
+            if (ysh_out) memcpy(ysh_out + (int64_t)n * d, y + (int64_t)k * d, sizeof(uint16_t) * d);
+        }
         for (int c = 0; c < d; ++c) {
             double acc = 0.0;
             for (int j = 0; j < k; ++j)
                 acc += (double)w[(int64_t)t * k + j] * orc_bf16_to_f64(y[(int64_t)j * d + c]);
-            if (F_sh > 0) acc += orc_bf16_to_f64(y[(int64_t)k * d + c]);
+            if (F_sh > 0)
+                acc += (sgate ? (double)sgate[t] : 1.0) * orc_bf16_to_f64(y[(int64_t)k * d + c]);
             out[(int64_t)n * d + c] = orc_bf16_from_f64(acc);
         }
         free(hbuf);

@@ -37,7 +37,7 @@ class tg_config(ctypes.Structure):
     _fields_ = [("d_model", ctypes.c_int), ("n_experts", ctypes.c_int), ("top_k", ctypes.c_int),
                 ("d_ffn", ctypes.c_int), ("d_ffn_shared", ctypes.c_int), ("n_ews", ctypes.c_int),
                 ("ew_rank", ctypes.POINTER(ctypes.c_int32)), ("slots_per_ew", ctypes.c_int),
-                ("max_tokens_per_rank", ctypes.c_int)]
+                ("max_tokens_per_rank", ctypes.c_int), ("gate_mode", ctypes.c_int), ("shared_gate", ctypes.c_int)]
 
 
 _lib = ctypes.CDLL(LIB_PATH)
@@ -50,6 +50,7 @@ _SIG = {
     "tg_load_gate": ([_P, _P, _I], _I),
     "tg_load_experts": ([_P, _I, _I, _I, _P, _P, _P, _I], _I),
     "tg_load_shared": ([_P, _P, _P, _P, _I], _I),
+    "tg_load_shared_gate": ([_P, _P, _I], _I),
     "tg_set_route_table": ([_P, _U64, _P, _I], _I),
     "tg_mask_worker": ([_P, _I, _I], _I),
     "tg_moe_layer": ([_P, _P, _P, _I, _P], _I),
@@ -110,13 +111,13 @@ def tg_last_error(ctx) -> str:
 
 
 def tg_init(d_model, n_experts, top_k, d_ffn, n_ews, ew_rank: Sequence[int], slots_per_ew,
-            max_tokens_per_rank, rank=0, world=1, device=None, d_ffn_shared=0):
+            max_tokens_per_rank, rank=0, world=1, device=None, d_ffn_shared=0, gate_mode=0, shared_gate=0):
     """Create a ctx; device=None -> torch.cuda.current_device(); device=-1 -> host-only ctx."""
     if device is None:
         device = torch.cuda.current_device() if torch.cuda.is_available() else -1
     ew = (ctypes.c_int32 * len(ew_rank))(*ew_rank)
     cfg = tg_config(d_model, n_experts, top_k, d_ffn, d_ffn_shared, len(ew_rank), ew, slots_per_ew,
-                    max_tokens_per_rank)
+                    max_tokens_per_rank, gate_mode, shared_gate)
     h = _P()
     rc = _lib.tg_init(ctypes.byref(cfg), rank, world, device, ctypes.byref(h))
     _check(None, rc, "tg_init")
@@ -149,6 +150,10 @@ def tg_load_experts(ctx, ew, slot, expert_id, w1, w3, w2):
 
 def tg_load_shared(ctx, w1, w3, w2):
     _check(ctx, _lib.tg_load_shared(ctx, _ptr(w1), _ptr(w3), _ptr(w2), int(w1.is_cuda)), "tg_load_shared")
+
+
+def tg_load_shared_gate(ctx, wsg):
+    _check(ctx, _lib.tg_load_shared_gate(ctx, _ptr(wsg), int(wsg.is_cuda)), "tg_load_shared_gate")
 
 
 def tg_set_route_table(ctx, version: int, cand: np.ndarray) -> int:
@@ -262,7 +267,8 @@ class MoELayer:
         self.device = torch.cuda.current_device() if device is None else device
         self.ctx = tg_init(shape.d, shape.E, shape.k, shape.F, placement.n_ews, placement.ew_rank,
                            placement.slots_per_ew, max_tokens_per_rank, rank, world, self.device,
-                           d_ffn_shared=shape.F_sh)
+                           d_ffn_shared=shape.F_sh, gate_mode=getattr(shape, "gate_mode", 0),
+                           shared_gate=getattr(shape, "shared_gate", 0))
         if world > 1:
             import torch.distributed as dist
             h = tg_get_peer_handle(self.ctx)
@@ -285,6 +291,8 @@ class MoELayer:
                     tg_load_experts(self.ctx, ew, sl, e, None, None, None)
         if shape.F_sh:
             tg_load_shared(self.ctx, *(w.contiguous() for w in weights.shared))
+        if getattr(shape, "shared_gate", 0):
+            tg_load_shared_gate(self.ctx, weights.wsg.contiguous())
         self.version = 0
         self.set_route_table(placement.cand, version)
         self.S_max = tg_max_slots(self.ctx)

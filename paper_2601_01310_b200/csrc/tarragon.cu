@@ -47,6 +47,8 @@ PFN_encodeTiled get_encode() {
 struct tg_ctx {
   // ---- config
   int d, E, k, F, Fsh, W, spe, T_max;
+  int gate_mode = 0, shared_gate = 0;
+  bool sgate_loaded = false;
   int rank, world, device;
   std::vector<int32_t> ew_rank, ew_base;  // per EW: rank, first bank slot on its rank
   std::vector<int> S_of_rank;             // bank slots per rank
@@ -168,8 +170,12 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
     return fail(nullptr, TG_ERR_INVALID, "rank %d / world %d (world <= %d)", rank, world, kMaxWorld);
   if (cfg->n_ews < 1 || !cfg->ew_rank || cfg->slots_per_ew < 1 || cfg->max_tokens_per_rank < 0)
     return fail(nullptr, TG_ERR_INVALID, "placement: n_ews, ew_rank, slots_per_ew, max_tokens_per_rank");
+  if (cfg->gate_mode < 0 || cfg->gate_mode > 1 || cfg->shared_gate < 0 || cfg->shared_gate > 1 ||
+      (cfg->shared_gate && Fsh == 0) || (cfg->shared_gate && E + 1 > kMaxExperts))
+    return fail(nullptr, TG_ERR_INVALID, "gate_mode must be 0/1; shared_gate 0/1 and needs d_ffn_shared > 0");
   c = new tg_ctx();
   c->d = d; c->E = E; c->k = k; c->F = F; c->Fsh = Fsh;
+  c->gate_mode = cfg->gate_mode; c->shared_gate = cfg->shared_gate;
   c->W = cfg->n_ews; c->spe = cfg->slots_per_ew; c->T_max = cfg->max_tokens_per_rank;
   c->rank = rank; c->world = world; c->device = cuda_device;
   c->ew_rank.assign(cfg->ew_rank, cfg->ew_rank + c->W);
@@ -223,7 +229,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   CKI(cudaMalloc(&c->bank_w1, S_loc * F * d * 2));
   CKI(cudaMalloc(&c->bank_w3, S_loc * F * d * 2));
   CKI(cudaMalloc(&c->bank_w2, S_loc * F * d * 2));
-  CKI(cudaMalloc(&c->wg, (size_t)E * d * 2));
+  CKI(cudaMalloc(&c->wg, (size_t)(E + 1) * d * 2));  // + shared-gate row
   if (Fsh > 0) {
     CKI(cudaMalloc(&c->w1s, (size_t)Fsh * d * 2));
     CKI(cudaMalloc(&c->w3s, (size_t)Fsh * d * 2));
@@ -252,8 +258,9 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   c->args.n_ctr_max = nt_max * (1 + ctiles) + nt_sh + 16;
   size_t so = 0;
   auto carve = [&](size_t bytes) { size_t o = so; so = align_up(so + bytes, 256); return o; };
+  size_t o_sg = carve(Tm * 4);
   size_t o_idx = carve(Tm * k * 4), o_w = carve(Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
-  size_t o_lp = carve(((Tm + 31) / 32) * (size_t)(d / 64) * 32 * E * 4);  // groups * nkp * 32 * E floats (KP >= 64)
+  size_t o_lp = carve(((Tm + 31) / 32) * (size_t)(d / 64) * 32 * (E + 1) * 4);  // groups * nkp * 32 * E floats (KP >= 64)
   size_t o_gc2 = carve(((Tm + 31) / 32) * 4);
   size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
   size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
@@ -280,7 +287,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
     const char *e = getenv("TG_L2PF");  // development override (bytes; 0 = off)
     a.l2_prefetch_bytes = e ? atoll(e) : (long long)(prop.l2CacheSize * 0.4);
   }
-  a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.key = (int32_t *)(sb + o_key);
+  a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.sgate = (float *)(sb + o_sg);
+  a.gate_mode = c->gate_mode; a.shared_gate = c->shared_gate; a.E_r = E + c->shared_gate; a.key = (int32_t *)(sb + o_key);
   a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
   a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
   a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
@@ -374,6 +382,17 @@ tg_status tg_load_gate(tg_ctx *c, const void *wg, int on_dev) {
     if (s) return s;
   }
   c->gate_loaded = true;
+  return TG_OK;
+}
+
+tg_status tg_load_shared_gate(tg_ctx *c, const void *wsg, int on_dev) {
+  if (!c || !wsg) return TG_ERR_INVALID;
+  if (!c->shared_gate) return fail(c, TG_ERR_INVALID, "config has shared_gate = 0");
+  if (!c->host_only) {
+    tg_status s = copy_in(c, reinterpret_cast<uint8_t *>(c->wg) + (size_t)c->E * c->d * 2, wsg, (size_t)c->d * 2, on_dev);
+    if (s) return s;
+  }
+  c->sgate_loaded = true;
   return TG_OK;
 }
 
@@ -478,6 +497,7 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
     return fail(c, TG_ERR_INVALID, "x/out must be 16-byte aligned");
   if (!c->gate_loaded) return fail(c, TG_ERR_NOT_LOADED, "router weights not loaded (tg_load_gate)");
   if (c->Fsh > 0 && !c->shared_loaded) return fail(c, TG_ERR_NOT_LOADED, "shared expert not loaded");
+  if (c->shared_gate && !c->sgate_loaded) return fail(c, TG_ERR_NOT_LOADED, "shared-expert gate not loaded");
   if (!c->have_table) return fail(c, TG_ERR_NOT_LOADED, "no route table (tg_set_route_table)");
   if (c->no_route) return fail(c, TG_ERR_NO_ROUTE, "some expert has no unmasked candidate: nothing launched");
   for (int q = 0; q < c->world; ++q)

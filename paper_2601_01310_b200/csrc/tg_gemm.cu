@@ -549,11 +549,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (a.Fsh > 0) {
       uint4 v = __ldcg(reinterpret_cast<const uint4 *>(a.ysh + (size_t)t * a.d) + c8);
       const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&v);
+      if (a.shared_gate) {  // shared expert scaled by sigmoid(x . wsg)
+        const float sg = __ldcg(a.sgate + t);
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        float2 f = __bfloat1622float2(vp[qq]);
-        acc[2 * qq] = __fadd_rn(acc[2 * qq], f.x);
-        acc[2 * qq + 1] = __fadd_rn(acc[2 * qq + 1], f.y);
+        for (int qq = 0; qq < 4; ++qq) {
+          float2 f = __bfloat1622float2(vp[qq]);
+          acc[2 * qq] = __fmaf_rn(sg, f.x, acc[2 * qq]);
+          acc[2 * qq + 1] = __fmaf_rn(sg, f.y, acc[2 * qq + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          float2 f = __bfloat1622float2(vp[qq]);
+          acc[2 * qq] = __fadd_rn(acc[2 * qq], f.x);
+          acc[2 * qq + 1] = __fadd_rn(acc[2 * qq + 1], f.y);
+        }
       }
     }
     uint4 o;

@@ -83,6 +83,9 @@ constexpr int FLAG_CNT = 0, FLAG_DATA = 1, FLAG_COMB = 2;
 struct CallArgs {
   // shape
   int d, E, k, F, Fsh, world, rank, S_max, S_loc, nkeys, T_max, R_cap, R_sh0, nsplit;
+  int E_r;               // router rows: E experts (+ 1 shared-gate row when shared_gate)
+  int gate_mode;         // 0: softmax over the selected k; 1: softmax over all E, not renormalised
+  int shared_gate;       // 1: shared expert scaled by sigmoid(x . wsg)
   int T;                 // tokens on this rank for this call
   int bn, nstages, stage_bytes;  // GEMM token-tile width and stage ring geometry of this call
   int g2dual;            // GEMM2 units cover two 128-row W2 tiles sharing one H tile (prefill-sized calls)
@@ -96,6 +99,7 @@ struct CallArgs {
   // per-call scratch (local)
   int32_t *idx;          // [T_max][k]
   float *w;              // [T_max][k]
+  float *sgate;          // [T_max] shared-expert weight per token (shared_gate)
   int32_t *key;          // [T_max][k] destination key of each pair
   int32_t *lrank;        // [T_max][k] rank of the pair within its block and key
   float *logit_part;     // [ceil(T_max/32)][nkp][32][E] router partial logits

@@ -91,16 +91,16 @@ __device__ __forceinline__ void stage_rows(uint32_t *dst, int ldw, int nrows, in
 }
 
 __device__ void router_stage_wg(const CallArgs &a, const RouterSmem &R, int kp) {
-  const int KP = router_kpart(a.d, a.E);
-  const int E8 = (a.E + 7) / 8 * 8;  // rows of the n8 tiles actually used
+  const int KP = router_kpart(a.d, a.E_r);
+  const int E8 = (a.E_r + 7) / 8 * 8;  // rows of the n8 tiles actually used
   stage_rows(R.wg, R.ldw, E8, KP / 8, [&](int e) -> const uint4 * {
-    return e < a.E ? reinterpret_cast<const uint4 *>(a.wg + (size_t)e * a.d + kp * KP) : nullptr;
+    return e < a.E_r ? reinterpret_cast<const uint4 *>(a.wg + (size_t)e * a.d + kp * KP) : nullptr;
   });
 }
 
 __device__ void router_item(const CallArgs &a, const RouteKeys &rk, const RouterSmem &R, int grp, int kp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = a.d, E = a.E, T = a.T;
+  const int d = a.d, E = a.E_r, T = a.T;  // router rows: experts (+ shared-gate row)
   const int g = lane >> 2, c = lane & 3;
   const int KP = router_kpart(d, E), nkp = router_nkp(d, E), Epad = router_epad(E);
   const int t0 = grp * kRouterRows;
@@ -188,23 +188,23 @@ __device__ void router_item(const CallArgs &a, const RouteKeys &rk, const Router
 // w_j = z_j / Z (IEEE).
 __device__ void topk_warp(const CallArgs &a, const RouteKeys &rk, int t, float *l) {
   const int lane = threadIdx.x & 31;
-  const int E = a.E, k = a.k;
-  const int nkp = router_nkp(a.d, E);
+  const int E = a.E, Er = a.E_r, k = a.k;
+  const int nkp = router_nkp(a.d, Er);
   const int grp = t / kRouterRows, row = t % kRouterRows;
-  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * E + row * E;
-  const int nw = (E + 31) / 32;  // <= 8 experts per lane
+  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * Er + row * Er;
+  const int nw = (Er + 31) / 32;  // <= 8 router rows per lane
   float val[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     val[i] = 0.f;
     const int e = lane + 32 * i;
-    if (i < nw && e < E) {
+    if (i < nw && e < Er) {
       float p[8];
       float s = 0.f;
       for (int q0 = 0; q0 < nkp; q0 += 8) {
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          p[u] = (q0 + u < nkp) ? __ldcg(src + (size_t)(q0 + u) * kRouterRows * E + e) : 0.f;
+          p[u] = (q0 + u < nkp) ? __ldcg(src + (size_t)(q0 + u) * kRouterRows * Er + e) : 0.f;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (q0 + u < nkp) s = (q0 + u == 0) ? p[u] : s + p[u];
@@ -247,14 +247,30 @@ __device__ void topk_warp(const CallArgs &a, const RouteKeys &rk, int t, float *
 #pragma unroll
   for (int i = 0; i < 8; ++i) z[i] = (slot_of[i] >= 0) ? expf(val[i] - m) : 0.f;
   float Z = 0.f;
-  for (int j = 0; j < k; ++j) {  // fixed slot order
-    float zj = 0.f;
+  if (a.gate_mode == 0) {
+    for (int j = 0; j < k; ++j) {  // fixed slot order
+      float zj = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const unsigned int b = __ballot_sync(0xffffffffu, slot_of[i] == j);
+        if (b) zj = __shfl_sync(0xffffffffu, z[i], __ffs(b) - 1);
+      }
+      Z = (j == 0) ? zj : Z + zj;
+    }
+  } else {
+    // gate_mode 1: full-softmax denominator over all E (m = max of all logits = top-1),
+    // per-lane sums in ascending i, then a fixed xor butterfly: deterministic, row-invariant
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const unsigned int b = __ballot_sync(0xffffffffu, slot_of[i] == j);
-      if (b) zj = __shfl_sync(0xffffffffu, z[i], __ffs(b) - 1);
+      const int e = lane + 32 * i;
+      if (i < nw && e < E) Z += (slot_of[i] >= 0) ? z[i] : expf(val[i] - m);
     }
-    Z = (j == 0) ? zj : Z + zj;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
+  }
+  if (a.shared_gate && lane == 0) {  // row E of the router: shared-expert gate logit
+    const float g = l[E];
+    a.sgate[t] = __fdiv_rn(1.0f, 1.0f + expf(-g));
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -447,7 +463,7 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
   TG_STAMP(8);
   const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
   {
-    const int nkp = router_nkp(a.d, a.E), KP = router_kpart(a.d, a.E), Epad = router_epad(a.E);
+    const int nkp = router_nkp(a.d, a.E_r), KP = router_kpart(a.d, a.E_r), Epad = router_epad(a.E_r);
     RouterSmem R;
     R.ldw = KP / 2 + 4;
     R.wg = reinterpret_cast<uint32_t *>(fsm);
@@ -471,7 +487,7 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
   // ---- P1b top-k + softmax + ERT key, one warp per token over the whole grid
   {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    float *lrow = reinterpret_cast<float *>(fsm) + (threadIdx.x >> 5) * a.E;
+    float *lrow = reinterpret_cast<float *>(fsm) + (threadIdx.x >> 5) * a.E_r;
     for (int t = gw; t < a.T; t += nw) topk_warp(a, rk, t, lrow);
   }
   grid_barrier_z(gbar, nbar++, a.err);
@@ -537,9 +553,9 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
 }
 
 static size_t front_smem(const CallArgs &a) {
-  const int KP = router_kpart(a.d, a.E), ldw = KP / 2 + 4;
-  size_t r = sizeof(uint32_t) * (size_t)(router_epad(a.E) + kRouterRows) * ldw +
-             sizeof(float) * std::max(8 * kRouterRows * 64, kRouterRows * (a.E + 1));
+  const int KP = router_kpart(a.d, a.E_r), ldw = KP / 2 + 4;
+  size_t r = sizeof(uint32_t) * (size_t)(router_epad(a.E_r) + kRouterRows) * ldw +
+             sizeof(float) * std::max(8 * kRouterRows * 64, kRouterRows * (a.E_r + 1));
   size_t b = sizeof(uint32_t) * 8 * a.nkeys;
   size_t e = sizeof(int32_t) * 3 * a.nkeys;
   return std::max(r, std::max(b, e));

@@ -207,3 +207,10 @@ def test_ds_v2_lite_shared_parity():
 def test_qwen_prefill_parity():
     """configs[4] shape: 60 experts top-4, prefill T = 8192 (multi-tile slots)."""
     _big("qwen_prefill", 2003, n_sample=48, W=4)
+
+
+@pytest.mark.parametrize("cfg,W", [("ds_v2_lite_decode_g1", 8), ("qwen_prefill_sg", 4)])
+def test_next3b_gating_variants(cfg, W):
+    """NEXT-3b: the public DS-V2-Lite / Qwen1.5-MoE gating (softmax over all E, top-k weights not
+    renormalised) and Qwen's sigmoid-gated shared expert (F_sh 5632), parity + mask bit-identity."""
+    _big(cfg, 2005, n_sample=32, W=W)

@@ -104,6 +104,51 @@ def test_softmax_closed_forms():
     assert gap[0] == np.float32(3.0)
 
 
+def test_gate_mode1_is_full_softmax_then_topk():
+    """O3' (gate_mode 1, NEXT-3b): w = softmax over all E (torch fp64), gathered at the selected ids,
+    not renormalised; k = E reduces bitwise to gate_mode 0 (the renormalised softmax of all E)."""
+    rng = np.random.default_rng(21)
+    l = rng.standard_normal((500, 60)).astype(np.float32)
+    for k in (1, 4, 6):
+        idx, w, _ = oracle.select(l, k, gate_mode=1)
+        idx0, _, _ = oracle.select(l, k, gate_mode=0)
+        assert np.array_equal(idx, idx0)                       # selection unchanged
+        full = torch.softmax(torch.from_numpy(l).double(), dim=1)
+        ref = torch.gather(full, 1, torch.from_numpy(idx).long()).float().numpy()
+        np.testing.assert_array_equal(w, ref)
+        assert np.all(w.astype(np.float64).sum(1) < 1.0 + 1e-6)
+    l8 = l[:, :8].copy()
+    np.testing.assert_array_equal(oracle.select(l8, 8, gate_mode=1)[1], oracle.select(l8, 8, gate_mode=0)[1])
+
+
+def test_shared_gate_closed_forms():
+    """O7' (NEXT-3b): wsg = 0 -> sigmoid(0) = 0.5 exactly -> out = y_sh / 2 bitwise (routed experts zero);
+    a gate logit >= 20 -> weight 1.0f -> out = y_sh bitwise; sigmoid matches torch in fp64."""
+    d, F, T, E = 32, 64, 24, 4
+    ws = _rand_expert(d, 48, 51)
+    z = np.zeros((F, d), np.uint16)
+    x = torch.randint(-2, 3, (T, d), generator=torch.Generator().manual_seed(52)).to(torch.bfloat16)
+    pl = wl.make_placement(E, 1, 1, shadows=False)
+    y_sh = _torch_swiglu_bf16(x, *ws)
+
+    def run(wsg):
+        return oracle.layer(wl.as_u16(x), np.zeros((E, d), np.uint16), 2, [z] * E, [z] * E,
+                            [np.zeros((d, F), np.uint16)] * E, pl.cand, pl.ew_rank, pl.slots_per_ew,
+                            np.zeros(1, np.uint8), G=1, shared=tuple(wl.as_u16(a) for a in ws),
+                            wsg=wl.as_u16(wsg))
+    r = run(torch.zeros(d, dtype=torch.bfloat16))
+    assert np.all(r["sgate"] == np.float32(0.5))
+    half = bf16_rne_exact(bf16_bits_to_f64(y_sh) * 0.5)
+    np.testing.assert_array_equal(r["out"], half)
+    big = torch.full((d,), 64.0, dtype=torch.bfloat16)      # x has a nonzero entry per row w.h.p.
+    r = run(big)
+    g = (x.double() @ big.double()).float()
+    ok = g.numpy() >= 20
+    assert ok.sum() > 5
+    np.testing.assert_array_equal(r["sgate"], torch.sigmoid(g.double()).float().numpy())
+    np.testing.assert_array_equal(r["out"][ok], y_sh[ok])
+
+
 def test_softmax_sums_to_one_random():
     rng = np.random.default_rng(7)
     l = rng.standard_normal((2000, 60)).astype(np.float32)

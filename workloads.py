@@ -32,6 +32,8 @@ class Shape:
     F: int          # expert FFN width
     F_sh: int = 0   # merged shared-expert width (0 = none)
     T: int = 256    # global tokens per layer call
+    gate_mode: int = 0    # 0 softmax over the k selected; 1 softmax over all E, no renormalisation
+    shared_gate: int = 0  # 1: shared expert scaled by sigmoid(x . wsg)
 
 
 # BASELINE.json "configs" (index = position in that list).
@@ -40,6 +42,12 @@ CONFIGS = {
     "mixtral_decode": Shape("mixtral_decode", d=4096, E=8, k=2, F=14336, T=256),     # configs[1], [2]
     "ds_v2_lite_decode": Shape("ds_v2_lite_decode", d=2048, E=64, k=6, F=1408, F_sh=2816, T=1024),  # configs[3]
     "qwen_prefill": Shape("qwen_prefill", d=2048, E=60, k=4, F=1408, T=8192),        # configs[4]
+    # NEXT-3b: the public models' own gating (norm_topk_prob = false) and, for Qwen1.5-MoE-A2.7B,
+    # its sigmoid-gated shared expert (shared_expert_intermediate_size 5632)
+    "ds_v2_lite_decode_g1": Shape("ds_v2_lite_decode_g1", d=2048, E=64, k=6, F=1408, F_sh=2816, T=1024,
+                                  gate_mode=1),
+    "qwen_prefill_sg": Shape("qwen_prefill_sg", d=2048, E=60, k=4, F=1408, F_sh=5632, T=8192,
+                             gate_mode=1, shared_gate=1),
 }
 
 
@@ -69,6 +77,7 @@ class Layer:
     w3: List[torch.Tensor]           # E x [F, d]
     w2: List[torch.Tensor]           # E x [d, F]
     shared: Optional[tuple] = None   # (W1s [F_sh,d], W3s [F_sh,d], W2s [d,F_sh])
+    wsg: Optional[torch.Tensor] = None  # [d] shared-expert gate (shared_gate)
 
 
 def make_layer(shape: Shape, seed: int, device="cpu", skew: float = 0.0, u: Optional[torch.Tensor] = None) -> Layer:
@@ -87,7 +96,8 @@ def make_layer(shape: Shape, seed: int, device="cpu", skew: float = 0.0, u: Opti
         shared = (bf16_normal((Fs, d), d ** -0.5, seed * 1000 + 2, device),
                   bf16_normal((Fs, d), d ** -0.5, seed * 1000 + 3, device),
                   bf16_normal((d, Fs), Fs ** -0.5, seed * 1000 + 4, device))
-    return Layer(shape, wg, w1, w3, w2, shared)
+    wsg = bf16_normal((d,), d ** -0.5, seed * 1000 + 5, device) if shape.shared_gate else None
+    return Layer(shape, wg, w1, w3, w2, shared, wsg)
 
 
 def make_tokens(shape: Shape, seed: int, T: Optional[int] = None, device="cpu", skew_mu: float = 0.0,
