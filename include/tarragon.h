@@ -134,7 +134,18 @@ tg_status tg_set_route_table(tg_ctx *ctx, uint64_t version, const int32_t *cand,
  * fixed.  Host-only, O(E * max_cands).                                     */
 tg_status tg_mask_worker(tg_ctx *ctx, int ew, int masked);
 
-/* One MoE layer round trip (collective: every rank calls it, same order).
+/* Fail-stop a whole rank (masked = 1): its AW shard and every EW it hosts
+ * (§3.3; §5.2 "EWs tolerate AW failures": the surviving
+ * ranks proceed without the failed AW's tokens).  Every surviving rank makes
+ * the same call (SPMD); from the next tg_moe_layer on, the masked rank is
+ * never awaited, written or read, its counts are taken as zero, and its
+ * experts are served by shadows (TG_ERR_NO_ROUTE as for tg_mask_worker if
+ * some expert has none).  The masked rank must not call tg_moe_layer again;
+ * rejoining needs re-provisioning (new ctxs, out of scope):
+ * masked = 0 on a masked rank returns TG_ERR_UNSUPPORTED.  Host-only.      */
+tg_status tg_mask_rank(tg_ctx *ctx, int rank, int masked);
+
+/* One MoE layer round trip (collective: every live rank calls it, same order).
  * x: device bf16 [n_tokens][d] (this rank's tokens); out: device bf16
  * [n_tokens][d], must not alias x.  n_tokens <= max_tokens_per_rank (may be
  * 0).  Enqueued on `stream` (cudaStream_t; NULL = legacy default stream);

@@ -53,6 +53,7 @@ _SIG = {
     "tg_load_shared_gate": ([_P, _P, _I], _I),
     "tg_set_route_table": ([_P, _U64, _P, _I], _I),
     "tg_mask_worker": ([_P, _I, _I], _I),
+    "tg_mask_rank": ([_P, _I, _I], _I),
     "tg_moe_layer": ([_P, _P, _P, _I, _P], _I),
     "tg_moe_layer_host": ([_P, _P, _P, _I, _P], _I),
     "tg_get_routing": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
@@ -166,6 +167,12 @@ def tg_mask_worker(ctx, ew: int, masked: int = 1) -> int:
     """Returns TG_OK or TG_ERR_NO_ROUTE (warning: mask applied, some expert unroutable)."""
     rc = _lib.tg_mask_worker(ctx, ew, masked)
     return _check(ctx, rc, "tg_mask_worker", ok=(TG_OK, TG_ERR_NO_ROUTE))
+
+
+def tg_mask_rank(ctx, rank: int, masked: int = 1) -> int:
+    """Fail-stop a whole rank (AW + its EWs); returns TG_OK or TG_ERR_NO_ROUTE (warning)."""
+    rc = _lib.tg_mask_rank(ctx, rank, masked)
+    return _check(ctx, rc, "tg_mask_rank", ok=(TG_OK, TG_ERR_NO_ROUTE))
 
 
 def tg_moe_layer(ctx, x: torch.Tensor, out: torch.Tensor, stream=None) -> int:
@@ -306,6 +313,9 @@ class MoELayer:
 
     def mask_worker(self, ew, masked=1):
         return tg_mask_worker(self.ctx, ew, masked)
+
+    def mask_rank(self, rank, masked=1):
+        return tg_mask_rank(self.ctx, rank, masked)
 
     def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         if out is None:

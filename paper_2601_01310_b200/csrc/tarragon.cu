@@ -61,6 +61,7 @@ struct tg_ctx {
   uint64_t version = 0;
   bool have_table = false;
   std::vector<uint8_t> mask;              // [W]
+  uint32_t alive = 0xffffffffu;           // bit r: rank r alive (tg_mask_rank)
   std::vector<int32_t> rkey;              // [E] resolved key or -1
   bool no_route = true;
   bool gate_loaded = false, shared_loaded = false;
@@ -463,7 +464,31 @@ tg_status tg_set_route_table(tg_ctx *c, uint64_t version, const int32_t *cand, i
 tg_status tg_mask_worker(tg_ctx *c, int ew, int masked) {
   if (!c) return TG_ERR_INVALID;
   if (ew < 0 || ew >= c->W) return fail(c, TG_ERR_INVALID, "ew %d out of range", ew);
+  if (!masked && !((c->alive >> c->ew_rank[ew]) & 1u))
+    return fail(c, TG_ERR_UNSUPPORTED, "ew %d is on failed rank %d", ew, c->ew_rank[ew]);
   c->mask[ew] = masked ? 1 : 0;
+  resolve(c);
+  if (c->have_table && c->no_route) {
+    int e = 0;
+    while (e < c->E && c->rkey[e] >= 0) ++e;
+    return fail(c, TG_ERR_NO_ROUTE, "expert %d lost its last unmasked candidate", e);
+  }
+  return TG_OK;
+}
+
+tg_status tg_mask_rank(tg_ctx *c, int r, int masked) {
+  if (!c) return TG_ERR_INVALID;
+  if (r < 0 || r >= c->world) return fail(c, TG_ERR_INVALID, "rank %d out of range", r);
+  if (r == c->rank) return fail(c, TG_ERR_INVALID, "a rank cannot mask itself");
+  if (!masked) {
+    if (!((c->alive >> r) & 1u))
+      return fail(c, TG_ERR_UNSUPPORTED, "rank %d rejoin needs re-provisioning (re-create the ctxs)", r);
+    return TG_OK;
+  }
+  c->alive &= ~(1u << r);
+  // the process took its EWs down with it: fail-stop every EW on that rank
+  for (int w = 0; w < c->W; ++w)
+    if (c->ew_rank[w] == r) c->mask[w] = 1;
   resolve(c);
   if (c->have_table && c->no_route) {
     int e = 0;
@@ -501,7 +526,7 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   if (!c->have_table) return fail(c, TG_ERR_NOT_LOADED, "no route table (tg_set_route_table)");
   if (c->no_route) return fail(c, TG_ERR_NO_ROUTE, "some expert has no unmasked candidate: nothing launched");
   for (int q = 0; q < c->world; ++q)
-    if (!c->peer[q]) return fail(c, TG_ERR_PEER, "peer %d not connected (tg_connect_peers)", q);
+    if (!c->peer[q] && ((c->alive >> q) & 1u)) return fail(c, TG_ERR_PEER, "peer %d not connected (tg_connect_peers)", q);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(c->device));
   RouteKeys rk;
@@ -525,6 +550,7 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
     a.stage_bytes = wide ? 65536 : 49152;
   }
   a.trace = c->tracing ? c->trace : nullptr;
+  a.alive = c->alive;
   for (int q = 0; q < kMaxWorld; ++q) a.sym[q] = q < c->world ? c->peer[q] : nullptr;
   c->n_ev = 0;
   rec(c, s);

@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   grid_barrier(gbar, a.epoch, 1, 0, err);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 16] = globaltimer_ns();
-  if (blockIdx.x == 0 && threadIdx.x < a.world) {
+  if (blockIdx.x == 0 && threadIdx.x < a.world && ((a.alive >> threadIdx.x) & 1u)) {
     // every expert output this rank computed is in its source's combine buffer
     fence_scope(sys);
     uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[threadIdx.x] + a.L.flags) + FLAG_COMB * kMaxWorld + a.rank;

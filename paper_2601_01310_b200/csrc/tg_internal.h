@@ -87,6 +87,7 @@ struct CallArgs {
   int gate_mode;         // 0: softmax over the selected k; 1: softmax over all E, not renormalised
   int shared_gate;       // 1: shared expert scaled by sigmoid(x . wsg)
   int T;                 // tokens on this rank for this call
+  uint32_t alive;        // bit r: rank r participates (fail-stopped ranks are never awaited or written)
   int bn, nstages, stage_bytes;  // GEMM token-tile width and stage ring geometry of this call
   int g2dual;            // GEMM2 units cover two 128-row W2 tiles sharing one H tile (prefill-sized calls)
   uint32_t epoch;

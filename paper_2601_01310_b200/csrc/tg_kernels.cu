@@ -360,13 +360,14 @@ __device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
     for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[s];
     return;
   }
-  // all-gather: my totals -> cnt_all[par][rank][*] on every peer, then release flags
+  // all-gather: my totals -> cnt_all[par][rank][*] on every live peer, then release flags
   for (int q = 0; q < a.world; ++q) {
+    if (!((a.alive >> q) & 1u)) continue;
     int32_t *dst = reinterpret_cast<int32_t *>(a.sym[q] + a.L.cnt_all) + ((size_t)par * a.world + a.rank) * nkeys;
     for (int K = tid; K < nkeys; K += blockDim.x) dst[K] = tot[K];
   }
   __syncthreads();
-  if (tid < a.world) {
+  if (tid < a.world && ((a.alive >> tid) & 1u)) {
     fence_scope(sys);
     uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[tid] + a.L.flags) + FLAG_CNT * kMaxWorld + a.rank;
     st_release(fl, a.epoch, sys);
@@ -378,7 +379,7 @@ __device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
   for (int K = tid; K < nkeys; K += blockDim.x) {
     int g = 0, bl = 0;
     for (int src = 0; src < a.world; ++src) {
-      int c = __ldcg(A + (size_t)src * nkeys + K);
+      const int c = ((a.alive >> src) & 1u) ? __ldcg(A + (size_t)src * nkeys + K) : 0;  // dead: no rows
       if (src < a.rank) bl += c;
       g += c;
     }
@@ -397,7 +398,7 @@ __device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
   if (tid < a.world) {
     int to_me = 0, to_q = 0;
     for (int s = 0; s < a.S_max; ++s) {
-      to_me += __ldcg(A + (size_t)tid * nkeys + a.rank * a.S_max + s);
+      to_me += ((a.alive >> tid) & 1u) ? __ldcg(A + (size_t)tid * nkeys + a.rank * a.S_max + s) : 0;
       to_q += tot[tid * a.S_max + s];
     }
     a.need_src[tid] = to_me > 0;
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
     s_last = (atomicAdd(&a.sync[3], 1) == (int)gridDim.x - 1);
   }
   __syncthreads();
-  if (s_last && threadIdx.x < a.world) {
+  if (s_last && threadIdx.x < a.world && ((a.alive >> threadIdx.x) & 1u)) {
     fence_scope(sys);
     uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[threadIdx.x] + a.L.flags) + FLAG_DATA * kMaxWorld + a.rank;
     st_release(fl, a.epoch, sys);

@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--W", type=int, default=0, help="logical EWs (default = world)")
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--sample", type=int, default=0, help="oracle FFN on this many sampled tokens (0 = all)")
+    ap.add_argument("--rank-fail", action="store_true",
+                    help="fail-stop the last rank (tg_mask_rank) instead of the EW/flip checks")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -94,6 +96,10 @@ def main():
     if not torch.equal(out.view(torch.int16), out2.view(torch.int16)):
         ok = False
         msgs.append(f"rank {rank}: run-to-run differs")
+    if a.rank_fail:
+        ok = rank_fail_checks(a, tg, layer, pl, sh, W, rank, world, dev, out, run, msgs, rep) and ok
+        finish(ok, rank, rep, msgs, layer, dev)
+        return
     # mask EW1 (+ poison its slots on its rank) -> bit-identical
     ew = 1 % W
     layer.mask_worker(ew, 1)
@@ -136,6 +142,50 @@ def main():
         torch.cuda.synchronize()
         rep["cross_G_bit_identical"] = bool(torch.equal(o1.cpu().view(torch.int16), out_all.view(torch.int16)))
         one.close()
+    finish(ok, rank, rep, msgs, layer, dev)
+
+
+def rank_fail_checks(a, tg, layer, pl, sh, W, rank, world, dev, out, run, msgs, rep):
+    """NEXT-3a (§3.3, §5.2): the last rank fail-stops (stops calling the
+    layer; its EWs go with it).  The survivors mask it and keep serving: never waiting on it
+    (a wait would trap after the 4 s bounded timeout), never sending it rows, and producing
+    outputs for their own tokens bit-identical to the all-alive run (its experts are served by
+    their shadows on live ranks, R#8 column independence)."""
+    ok = True
+    dead = world - 1
+    dist.barrier()
+    if rank != dead:
+        rc = layer.mask_rank(dead)
+        if rc != tg.TG_OK:
+            return False
+        st0 = layer.stats()
+        for i in range(6):
+            o = run()
+            if not torch.equal(out.view(torch.int16), o.view(torch.int16)):
+                ok = False
+                msgs.append(f"rank {rank}: call {i} after rank {dead} failed differs "
+                            f"({int((out != o).sum())} elements)")
+        st1 = layer.stats() - st0
+        if int(st1[dead].sum()) != 0:
+            ok = False
+            msgs.append(f"rank {rank}: rows were sent to the failed rank")
+        # rejoin is re-provisioning (out of scope): refused
+        try:
+            layer.mask_rank(dead, 0)
+            ok = False
+            msgs.append(f"rank {rank}: unmask of a failed rank not refused")
+        except tg.TarragonError as e:
+            if e.status != tg.TG_ERR_UNSUPPORTED:
+                ok = False
+                msgs.append(f"rank {rank}: unmask refused with {e}")
+        rep["rank_fail_calls"] = 6
+    rep["rank_fail_dead"] = dead
+    # the failed process is still alive for the harness: it meets the survivors only here
+    dist.barrier()
+    return ok
+
+
+def finish(ok, rank, rep, msgs, layer, dev):
     flags = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flags)
     if rank == 0:

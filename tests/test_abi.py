@@ -87,6 +87,34 @@ def test_mask_semantics_host_only():
     tg.tg_finalize(ctx)
 
 
+def test_mask_rank_host_only():
+    """NEXT-3a: fail-stopping a rank masks every EW it hosts; experts keep a
+    route through shadows on live ranks; a rank cannot mask itself; rejoin is refused (re-provision)."""
+    tg, ctx, pl = _host_ctx(E=8, W=2, G=2, rank=0)
+    assert tg.tg_set_route_table(ctx, 1, pl.cand) == tg.TG_OK
+    with pytest.raises(tg.TarragonError):
+        tg.tg_mask_rank(ctx, 0, 1)                      # itself
+    with pytest.raises(tg.TarragonError):
+        tg.tg_mask_rank(ctx, 2, 1)                      # out of range
+    assert tg.tg_mask_rank(ctx, 1, 0) == tg.TG_OK       # unmask of a live rank: no-op
+    assert tg.tg_mask_rank(ctx, 1, 1) == tg.TG_OK       # every expert has a shadow on rank 0
+    with pytest.raises(tg.TarragonError) as ei:
+        tg.tg_mask_rank(ctx, 1, 0)
+    assert ei.value.status == tg.TG_ERR_UNSUPPORTED
+    with pytest.raises(tg.TarragonError) as ei:
+        tg.tg_mask_worker(ctx, 1, 0)                    # EW 1 lives on the failed rank
+    assert ei.value.status == tg.TG_ERR_UNSUPPORTED
+    # the failed rank's EWs are masked: a table routing only to them is rejected
+    prim_only = np.ascontiguousarray(pl.cand[:, :1, :])
+    assert tg.tg_set_route_table(ctx, 2, prim_only) == tg.TG_ERR_NO_ROUTE
+    tg.tg_finalize(ctx)
+    # two EWs per rank, shadows of EW 2's primaries partly on EW 3 (same rank): no route
+    tg, ctx, pl = _host_ctx(E=8, W=4, G=2, rank=0)
+    assert tg.tg_set_route_table(ctx, 1, pl.cand) == tg.TG_OK
+    assert tg.tg_mask_rank(ctx, 1, 1) == tg.TG_ERR_NO_ROUTE
+    tg.tg_finalize(ctx)
+
+
 def test_host_only_ctx_refuses_compute():
     """No CPU fallback: a host-only ctx returns TG_ERR_UNSUPPORTED from tg_moe_layer."""
     tg, ctx, pl = _host_ctx()

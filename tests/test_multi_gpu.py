@@ -36,3 +36,12 @@ def test_tiny_multi_gpu(W_mult):
 def test_mixtral_multi_gpu():
     G = torch.cuda.device_count()
     _run(G, "--config", "mixtral_decode", "--sample", "16")
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("config", ["tiny", "mixtral_decode"])
+def test_rank_fail_stop(config):
+    """NEXT-3a: a whole rank fail-stops; survivors keep serving bit-identically."""
+    G = torch.cuda.device_count()
+    rep = _run(G, "--config", config, "--rank-fail")
+    assert rep["rank_fail_dead"] == G - 1
