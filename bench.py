@@ -51,14 +51,44 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled every ~2 ms during the timed region (NVML, read in a
+    thread; nvidia-smi -lms 10 as the fallback when NVML is unavailable)."""
+
+    _NVML_BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                  "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
         self.proc = None
+        self.stop = threading.Event()
+        self.nvml = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        try:  # CUDA and NVML orders can differ: match the PCI location of the CUDA device
+            pr = torch.cuda.get_device_properties(self.index)
+            want = (int(pr.pci_domain_id), int(pr.pci_bus_id), int(pr.pci_device_id))
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                hi = pynvml.nvmlDeviceGetHandleByIndex(i)
+                pi = pynvml.nvmlDeviceGetPciInfo(hi)
+                if (int(pi.domain), int(pi.bus), int(pi.device)) == want:
+                    h = hi
+                    break
+        except Exception:
+            pass
+        return pynvml, h
 
     def __enter__(self):
+        try:
+            self.nvml = self._nvml_handle()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         q = "clocks.sm,clocks.max.sm," + ",".join("clocks_event_reasons." + r for r in REASONS)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
@@ -71,11 +101,28 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv, h = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx)] + ["Active" if bits & self._NVML_BITS[r] else "Not Active"
+                                                          for r in REASONS])
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.samples.append([s.strip() for s in line.split(",")])
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
+            return
         if self.proc is not None:
             time.sleep(0.1)
             self.proc.terminate()
@@ -98,7 +145,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(active),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def dist_env():
@@ -324,7 +371,12 @@ def main():
         Lh = wl.Layer(shape, L.wg.cpu(), [w.cpu() for w in L.w1], [w.cpu() for w in L.w3],
                       [w.cpu() for w in L.w2], tuple(w.cpu() for w in L.shared) if L.shared else None,
                       L.wsg.cpu() if L.wsg is not None else None)
-        v, dt = cpu_oracle_sample(shape, Lh, xs[0].cpu(), pl, n, cores)
+        xc = xs[0].cpu()
+        v, dt = cpu_oracle_sample(shape, Lh, xc, pl, n, cores)
+        if args.cpu_sample is None and dt < 8.0:
+            # scale the sample to ~12 s of CPU work (bounded by the batch)
+            n = int(min(xc.shape[0], max(n, n * 12.0 / max(dt, 1e-3))))
+            v, dt = cpu_oracle_sample(shape, Lh, xc, pl, n, cores)
         cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                "sample": f"first {n} tokens of one batch through O1-O8 (fp64, {cores} threads over tokens), "
                          f"{dt:.1f} s"}

@@ -238,7 +238,8 @@ def tg_get_trace(ctx, cap=1 << 20):
                 kind=((t >> np.uint64(12)) & np.uint64(0xF)).astype(np.int64),
                 smid=(t & np.uint64(0xFFF)).astype(np.int64),
                 start=(tr[nu:nu + nc] & m48).astype(np.int64),
-                front_stamps=(tr[nu + 148:nu + 148 + 40] & m48).astype(np.int64),
+                front_stamps=(tr[nu + 148:nu + 148 + 64] & m48).astype(np.int64),
+                front_stamps_raw=tr[nu + 148:nu + 148 + 64].astype(np.int64),
                 front_block_p1=(tr[nu + 148 + 64:nu + 148 + 64 + 148] & m48).astype(np.int64),
                 topk_cycles=tr[nu + 148 + 64 + 256:nu + 148 + 64 + 256 + 296].astype(np.int64).reshape(148, 2))
 

@@ -82,6 +82,7 @@ struct tg_ctx {
   bool tracing = false;
   int force_mode = -1;                           // TG_WIDE=0/1 (development A/B), -1 auto
   int force_dual = -1;                           // TG_G2DUAL=0/1 (development A/B), -1 auto
+  bool skip_gemm = false;                        // TG_SKIP_GEMM=1: front only (development timing, wrong outputs)
   bf16 *x_stage = nullptr, *out_stage = nullptr;   // for tg_moe_layer_host
   uint32_t epoch = 0;
   int last_T = 0;
@@ -262,7 +263,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t o_sg = carve(Tm * 4);
   size_t o_idx = carve(Tm * k * 4), o_w = carve(Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
   size_t o_lp = carve(((Tm + 31) / 32) * (size_t)(d / 64) * 32 * (E + 1) * 4);  // groups * nkp * 32 * E floats (KP >= 64)
-  size_t o_gc2 = carve(((Tm + 31) / 32) * 4);
+  size_t o_gc2 = carve(((Tm + 31) / 32) * 4), o_cc = carve((size_t)(1 + nblk_max) * 4);
   size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
   size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
   size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(64);
@@ -290,7 +291,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   }
   a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.sgate = (float *)(sb + o_sg);
   a.gate_mode = c->gate_mode; a.shared_gate = c->shared_gate; a.E_r = E + c->shared_gate; a.key = (int32_t *)(sb + o_key);
-  a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
+  a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.chunk_ctr = (int32_t *)(sb + o_cc); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
   a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
   a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
   a.sync = (int32_t *)(sb + o_sync); a.ctr = (int32_t *)(sb + o_ctr);
@@ -306,6 +307,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
     if (wm && (wm[0] == '0' || wm[0] == '1')) c->force_mode = wm[0] - '0';
     const char *dm = getenv("TG_G2DUAL");
     if (dm && (dm[0] == '0' || dm[0] == '1')) c->force_dual = dm[0] - '0';
+    const char *sg = getenv("TG_SKIP_GEMM");
+    c->skip_gemm = sg && sg[0] == '1';
   }
   CKI(cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
   *c->err_host = 0;
@@ -556,7 +559,7 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   rec(c, s);
   CK(launch_front(a, rk, c->n_sms, s));
   rec(c, s);
-  CK(launch_gemm(a, c->maps, c->n_sms, s));
+  if (!c->skip_gemm) CK(launch_gemm(a, c->maps, c->n_sms, s));
   rec(c, s);
   if (c->prof) ++c->prof_calls;
   c->last_T = T;

@@ -104,7 +104,8 @@ struct CallArgs {
   int32_t *key;          // [T_max][k] destination key of each pair
   int32_t *lrank;        // [T_max][k] rank of the pair within its block and key
   float *logit_part;     // [ceil(T_max/32)][nkp][32][E] router partial logits
-  int32_t *grp_ctr;      // [ceil(T_max/32)] K-part arrival counters (zeroed in P2 of each call)
+  int32_t *grp_ctr;      // [ceil(T_max/32)] K-part arrival counters (reset by the last arriver)
+  int32_t *chunk_ctr;    // [1 + ceil(T_max/256)]: [0] chunks ranked, [1 + c] groups of chunk c done
   int32_t *bcnt;         // [nblk_max][nkeys] per-block counts -> exclusive block bases
   int32_t *dbase;        // [nkeys] base row of this source in each (rank, slot)
   int32_t *dst_pos;      // [T_max][k]

@@ -31,6 +31,11 @@ namespace tg {
       a.trace[a.n_units_max + 148 + (i)] = globaltimer_ns();                            \
   } while (0)
 
+#define TG_STAMP_ANY(i)                                                                 \
+  do {                                                                                  \
+    if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + (i)] = globaltimer_ns(); \
+  } while (0)
+
 // --------------------------------------------------------------------- P1
 // Router logits on tensor cores.  The K dimension is cut into parts of KP
 // elements (a function of d and E only); block b owns part kp = b % nkp for
@@ -69,36 +74,30 @@ struct RouterSmem {
   int ldw;        // row stride in words
 };
 
-// Batched copy of rows of 16-B chunks into padded smem rows: 8 loads in flight per
+// Batched copy of rows of 16-B chunks into padded smem rows: 16 loads in flight per
 // thread before the stores (these loops are latency-bound, not bandwidth-bound).
-template <typename RowPtr>
-__device__ __forceinline__ void stage_rows(uint32_t *dst, int ldw, int nrows, int cpr, RowPtr row) {
+template <typename RowPtr, typename DstRow>
+__device__ __forceinline__ void stage_rows(int nrows, int cpr, RowPtr row, DstRow drow) {
   const int total = nrows * cpr;
-  for (int i0 = threadIdx.x; i0 < total; i0 += 8 * blockDim.x) {
-    uint4 v[8];
+  const int lc = __ffs(cpr) - 1;  // cpr = KP / 8 is a power of two
+#pragma unroll 1
+  for (int i0 = threadIdx.x; i0 < total; i0 += 16 * blockDim.x) {
+    uint4 v[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 16; ++u) {
       const int i = i0 + u * blockDim.x;
-      const uint4 *p = (i < total) ? row(i / cpr) : nullptr;
-      v[u] = p ? __ldg(p + i % cpr) : make_uint4(0, 0, 0, 0);
+      const uint4 *p = (i < total) ? row(i >> lc) : nullptr;
+      v[u] = p ? __ldg(p + (i & (cpr - 1))) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 16; ++u) {
       const int i = i0 + u * blockDim.x;
-      if (i < total) *reinterpret_cast<uint4 *>(dst + (i / cpr) * ldw + (i % cpr) * 4) = v[u];
+      if (i < total) *reinterpret_cast<uint4 *>(drow(i >> lc) + (i & (cpr - 1)) * 4) = v[u];
     }
   }
 }
 
-__device__ void router_stage_wg(const CallArgs &a, const RouterSmem &R, int kp) {
-  const int KP = router_kpart(a.d, a.E_r);
-  const int E8 = (a.E_r + 7) / 8 * 8;  // rows of the n8 tiles actually used
-  stage_rows(R.wg, R.ldw, E8, KP / 8, [&](int e) -> const uint4 * {
-    return e < a.E_r ? reinterpret_cast<const uint4 *>(a.wg + (size_t)e * a.d + kp * KP) : nullptr;
-  });
-}
-
-__device__ void router_item(const CallArgs &a, const RouteKeys &rk, const RouterSmem &R, int grp, int kp) {
+__device__ void router_item(const CallArgs &a, const RouterSmem &R, int grp, int kp, bool with_wg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = a.d, E = a.E_r, T = a.T;  // router rows: experts (+ shared-gate row)
   const int g = lane >> 2, c = lane & 3;
@@ -106,10 +105,16 @@ __device__ void router_item(const CallArgs &a, const RouteKeys &rk, const Router
   const int t0 = grp * kRouterRows;
   const int cpr = KP / 8;
   if (grp == 0 && kp == 0) TG_STAMP(10);
-  // x tile [32][KP] -> smem (rows past T clamped; their results are never used)
-  stage_rows(R.xt, R.ldw, kRouterRows, cpr, [&](int r) -> const uint4 * {
-    return reinterpret_cast<const uint4 *>(a.x + (size_t)min(t0 + r, T - 1) * d + kp * KP);
-  });
+  // x tile [32][KP] -> smem (rows past T clamped; their results are never used); on the
+  // block's first item the Wg slice [E8][KP] joins the same load batch (one latency)
+  const int E8 = with_wg ? (E + 7) / 8 * 8 : 0;  // Wg rows of the n8 tiles actually used
+  stage_rows(
+      E8 + kRouterRows, cpr,
+      [&](int r) -> const uint4 * {
+        if (r < E8) return r < E ? reinterpret_cast<const uint4 *>(a.wg + (size_t)r * d + kp * KP) : nullptr;
+        return reinterpret_cast<const uint4 *>(a.x + (size_t)min(t0 + r - E8, T - 1) * d + kp * KP);
+      },
+      [&](int r) -> uint32_t * { return (r < E8 ? R.wg + r * R.ldw : R.xt + (r - E8) * R.ldw); });
   __syncthreads();
   if (grp == 0 && kp == 0) TG_STAMP(11);
   const int ksw = max(16, KP / 8);   // K elements of this warp (multiple of 16)
@@ -186,105 +191,148 @@ __device__ void router_item(const CallArgs &a, const RouteKeys &rk, const Router
 // (slots in ascending expert id, R#4).  Softmax over the k selected:
 // m = max, z_j = expf(l_j - m), Z = ((z_0 + z_1) + ...) in slot order,
 // w_j = z_j / Z (IEEE).
-__device__ void topk_warp(const CallArgs &a, const RouteKeys &rk, int t, float *l) {
-  const int lane = threadIdx.x & 31;
-  const int E = a.E, Er = a.E_r, k = a.k;
-  const int nkp = router_nkp(a.d, Er);
-  const int grp = t / kRouterRows, row = t % kRouterRows;
-  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * Er + row * Er;
-  const int nw = (Er + 31) / 32;  // <= 8 router rows per lane
-  float val[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    val[i] = 0.f;
-    const int e = lane + 32 * i;
-    if (i < nw && e < Er) {
-      float p[8];
-      float s = 0.f;
-      for (int q0 = 0; q0 < nkp; q0 += 8) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          p[u] = (q0 + u < nkp) ? __ldcg(src + (size_t)(q0 + u) * kRouterRows * Er + e) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (q0 + u < nkp) s = (q0 + u == 0) ? p[u] : s + p[u];
-      }
-      val[i] = s;
-      l[e] = s;
-    }
-  }
-  __syncwarp();
-  int slot_of[8];
-  int below = 0;  // selected experts in lower 32-chunks
-  float m = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    slot_of[i] = -1;
-    if (i < nw) {
-      const int e = lane + 32 * i;
-      bool sel = false;
-      if (e < E) {
-        const float v = val[i];
-        int beat = 0;
-#pragma unroll 8
-        for (int e2 = 0; e2 < E; ++e2) {
-          const float v2 = l[e2];
-          beat += (v2 > v) || (v2 == v && e2 < e);
-        }
-        sel = beat < k;
-      }
-      const unsigned int bal = __ballot_sync(0xffffffffu, sel);
-      if (sel) {
-        slot_of[i] = below + __popc(bal & ((1u << lane) - 1u));
-        m = fmaxf(m, val[i]);
-      }
-      below += __popc(bal);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float z[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) z[i] = (slot_of[i] >= 0) ? expf(val[i] - m) : 0.f;
-  float Z = 0.f;
-  if (a.gate_mode == 0) {
-    for (int j = 0; j < k; ++j) {  // fixed slot order
-      float zj = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const unsigned int b = __ballot_sync(0xffffffffu, slot_of[i] == j);
-        if (b) zj = __shfl_sync(0xffffffffu, z[i], __ffs(b) - 1);
-      }
-      Z = (j == 0) ? zj : Z + zj;
-    }
-  } else {
-    // gate_mode 1: full-softmax denominator over all E (m = max of all logits = top-1),
-    // per-lane sums in ascending i, then a fixed xor butterfly: deterministic, row-invariant
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = lane + 32 * i;
-      if (i < nw && e < E) Z += (slot_of[i] >= 0) ? z[i] : expf(val[i] - m);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
-  }
-  if (a.shared_gate && lane == 0) {  // row E of the router: shared-expert gate logit
-    const float g = l[E];
-    a.sgate[t] = __fdiv_rn(1.0f, 1.0f + expf(-g));
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if (slot_of[i] >= 0) {
-      const int e = lane + 32 * i, j = slot_of[i];
-      a.idx[(size_t)t * k + j] = e;
-      a.w[(size_t)t * k + j] = __fdiv_rn(z[i], Z);
-      a.key[(size_t)t * k + j] = rk.key[e];
-    }
-  }
-  __syncwarp();
+// P1b for one 32-token group, by the block that delivered its last K part (or by
+// a grid-stride loop in phased mode).  Logits = sum of the parts in part order
+// (16 loads in flight per thread) into smem rows.  Top-k: 8 lanes per token (one
+// warp holds 4 tokens), k rounds of a warp arg-max under the strict total order
+// "(v, e) beats (v', e') iff v > v' or (v == v' and e < e')" — lowest id wins
+// ties, -0 == +0; NaN logits read as -inf — so round j picks the expert beaten
+// by exactly j others and the picks are {e : fewer than k experts beat e}.
+// Slots in ascending expert id (R#4); softmax over the k selected with m = top-1
+// logit, z_j = expf(l_j - m), Z = ((z_0 + z_1) + ...) in slot order (gate_mode
+// 0), or over all E as 8 per-lane ascending partial sums combined by a fixed xor
+// tree (gate_mode 1); w_j = z_j / Z (IEEE).  Every reduction order depends on
+// (E, k) only: deterministic and row-invariant.  (Latency matters here, not
+// work: short dependency chains, no branches in the scans.)
+__device__ __forceinline__ bool beats(float v, int e, float v2, int e2) {
+  return (v > v2) | ((v == v2) & (e < e2));
 }
 
-__device__ void rank_chunk(const CallArgs &a, int chunk, uint8_t *smraw) {
+
+// Top-k of one token on 8 lanes (sub = lane & 7 holds experts e = sub + 8 i,
+// i < PER, in registers): k rounds of arg-max (local chain, then a 3-level xor
+// tree within the 8 lanes); the owner marks its pick taken.  Lane j keeps the
+// j-th pick.
+template <int PER>
+__device__ __forceinline__ void topk_rows(const CallArgs &a, const RouteKeys &rk, int t0, bool act,
+                                          const float *l, int *rsl) {
+  const int E = a.E, k = a.k, lane = threadIdx.x & 31, sub = lane & 7;
+  const int r = threadIdx.x >> 3;
+  float v[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int e = sub + 8 * i;
+    float x = (act && e < E) ? l[e] : -INFINITY;
+    v[i] = (x != x) ? -INFINITY : x;
+  }
+  uint32_t taken = 0;
+  int mine = 0x7fffffff;
+  float mval = 0.f, m = 0.f;
+#pragma unroll 1
+  for (int j = 0; j < k; ++j) {
+    float bv = -INFINITY;
+    int be = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = sub + 8 * i;
+      const bool ok = (e < E) & !((taken >> i) & 1u) & beats(v[i], e, bv, be);
+      bv = ok ? v[i] : bv;
+      be = ok ? e : be;
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      const bool tk = beats(ov, oe, bv, be);
+      bv = tk ? ov : bv;
+      be = tk ? oe : be;
+    }
+    if ((be & 7) == sub) taken |= 1u << (be >> 3);
+    if (sub == j) { mine = be; mval = bv; }
+    if (j == 0) m = bv;  // top-1 logit = max of the selected
+  }
+  // slot = picks with a smaller id (ascending expert id, R#4)
+  int slot = 0;
+#pragma unroll 1
+  for (int jj = 0; jj < k; ++jj) slot += __shfl_sync(0xffffffffu, mine, (lane & ~7) + jj) < mine;
+  if (sub < k) rsl[slot] = mine;
+  __syncwarp();
+  float Z = 0.f;
+  if (a.gate_mode == 0) {
+#pragma unroll 1
+    for (int s = 0; act && s < k; ++s) {  // fixed slot order
+      const float zs = expf(l[rsl[s]] - m);
+      Z = (s == 0) ? zs : Z + zs;
+    }
+  } else {
+    // softmax over all E: per-lane partial sums in ascending i, then a fixed xor tree
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      if (sub + 8 * i < E) Z += expf(v[i] - m);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
+  }
+  if (act) {
+    const int t = t0 + r;
+    if (sub < k) {
+      const size_t o = (size_t)t * k + slot;
+      a.idx[o] = mine;
+      a.w[o] = __fdiv_rn(expf(mval - m), Z);
+      a.key[o] = rk.key[mine];
+    }
+    if (a.shared_gate && sub == 0) a.sgate[t] = __fdiv_rn(1.0f, 1.0f + expf(-l[E]));  // router row E
+  }
+}
+
+__device__ __forceinline__ void group_topk(const CallArgs &a, const RouteKeys &rk, int grp, float *sm) {
+  const int Er = a.E_r, E = a.E, nkp = router_nkp(a.d, Er), ld = Er + 1;  // padded rows
+  const int t0 = grp * kRouterRows, nrow = min(kRouterRows, a.T - t0);
+  const int n = nrow * Er;
+  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * Er;
+  float *lsum = sm;                                              // [32][Er + 1]
+  int *sl = reinterpret_cast<int *>(lsum + kRouterRows * ld);    // [32][kMaxK] selected ids by slot
+  const int bd = blockDim.x;
+#pragma unroll 1
+  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * bd) {
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int q0 = 0; q0 < nkp; q0 += 4) {
+      float p[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          p[u][q] = (i0 + u * bd < n && q0 + q < nkp)
+                        ? __ldcg(src + (size_t)(q0 + q) * kRouterRows * Er + i0 + u * bd) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q0 + q < nkp) s[u] = (q0 + q == 0) ? p[u][q] : s[u] + p[u][q];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * bd;
+      if (i < n) lsum[i + i / Er] = s[u];  // row i / Er, padded stride Er + 1
+    }
+  }
+  __syncthreads();
+  if (grp == 0) TG_STAMP_ANY(31);
+  // 256 threads = 32 tokens x 8; all lanes run every step (shuffles), writes are predicated
+  const int r = threadIdx.x >> 3;
+  const int per = (E + 7) / 8;
+  if (per <= 1) topk_rows<1>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
+  else if (per <= 2) topk_rows<2>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
+  else if (per <= 4) topk_rows<4>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
+  else if (per <= 8) topk_rows<8>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
+  else if (per <= 16) topk_rows<16>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
+  else topk_rows<32>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
+  if (grp == 0) TG_STAMP_ANY(37);
+  __syncthreads();
+  __syncthreads();
+}
+
+__device__ __forceinline__ void rank_chunk(const CallArgs &a, int chunk, uint8_t *smraw) {
   const int tid = threadIdx.x, nkeys = a.nkeys, k = a.k;
   uint32_t *bm = reinterpret_cast<uint32_t *>(smraw);  // [nkeys][8]
   const int t = chunk * kRankBlock + tid;
@@ -313,7 +361,7 @@ __device__ void rank_chunk(const CallArgs &a, int chunk, uint8_t *smraw) {
 }
 
 // --------------------------------------------------------------------- P3
-__device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
+__device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
   const int tid = threadIdx.x, nkeys = a.nkeys;
   int32_t *tot = sm;              // [nkeys] this rank's rows per key
   int32_t *gsum = sm + nkeys;     // [nkeys] rows per key over all sources
@@ -334,7 +382,7 @@ __device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
         }
     }
     tot[K] = run;
-    a.stats[K] += run;
+    atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + K), (unsigned long long)run);
   }
   __syncthreads();
   if (a.world == 1) {
@@ -407,6 +455,64 @@ __device__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
   for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[a.rank * a.S_max + s];
 }
 
+// ------------------------------------------------------- P1 -> P3 chaining
+// No grid barriers between P1, P1b, P2 and P3: the block that delivers the last
+// K part of a 32-token group runs its top-k (P1b); the block that completes the
+// last group of a 256-token chunk ranks the chunk (P2); the block that completes
+// the last chunk runs the count exchange (P3).  Arrival = __threadfence + atomic
+// counter (threadfence-reduction pattern); the last arriver resets the counter
+// for the next call (kernel boundaries order the calls).
+__device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, int nkp, int ngroups, float *sm) {
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int last = atomicAdd(a.grp_ctr + grp, 1) == nkp - 1;
+    if (last) {
+      a.grp_ctr[grp] = 0;
+      __threadfence();
+    }
+    s_last = last;
+  }
+  __syncthreads();
+  if (grp == 0 && a.trace && threadIdx.x == 0)
+    a.trace[a.n_units_max + 148 + 40 + (blockIdx.x % nkp)] = globaltimer_ns();  // arrival of each part
+  if (!s_last) return;
+  if (grp == 0) TG_STAMP_ANY(30);
+  group_topk(a, rk, grp, sm);
+  if (grp == 0) TG_STAMP_ANY(12);
+  constexpr int gpc = kRankBlock / kRouterRows;
+  const int ch = grp / gpc, nchunks = (a.T + kRankBlock - 1) / kRankBlock;
+  const int ng_ch = min(gpc, ngroups - ch * gpc);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int last = atomicAdd(a.chunk_ctr + 1 + ch, 1) == ng_ch - 1;
+    if (last) {
+      a.chunk_ctr[1 + ch] = 0;
+      __threadfence();
+    }
+    s_last = last;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  rank_chunk(a, ch, reinterpret_cast<uint8_t *>(sm));
+  if (ch == 0) TG_STAMP_ANY(13);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int last = atomicAdd(a.chunk_ctr, 1) == nchunks - 1;
+    if (last) {
+      a.chunk_ctr[0] = 0;
+      __threadfence();
+    }
+    s_last = last;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  TG_STAMP_ANY(1);
+  exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(sm));
+  TG_STAMP_ANY(14);
+  __syncthreads();
+}
+
 // --------------------------------------------------------------------- P4
 // Warp copy of one row of nch 16-B chunks: up to 16 loads of a lane in flight
 // before its stores (the copy is latency-bound per warp).
@@ -426,6 +532,30 @@ __device__ __forceinline__ void copy_row(uint4 *__restrict__ dst, const uint4 *_
   }
 }
 
+// L2 prefetch of the weights the GEMM streams first (block `part` of `nparts`
+// issues its share).  The GEMM takes its GEMM1 units slot by slot; the first
+// slot with rows is predicted from the previous call's per-slot counts (routing
+// is sticky across decode steps).  A wrong guess only costs idle HBM bandwidth
+// during this latency-bound kernel.  Issued after the router's own loads so the
+// HBM queues serve those first.
+__device__ void l2_prefetch_share(const CallArgs &a, int part, int nparts) {
+  // issued by warp 1: thread 0's __threadfence in the arrival must not wait for these
+  if (threadIdx.x != 32 || a.l2_prefetch_bytes <= 0) return;
+  int s0 = -1;
+  for (int s = 0; s < a.S_loc && s0 < 0; ++s)
+    if (__ldcg(a.slot_rows + s) > 0) s0 = s;
+  if (s0 < 0) return;
+  const long long per_mat = min((long long)a.F * a.d * 2, a.l2_prefetch_bytes / 2);  // W1 and W3 halves
+  const long long chunk = 65536;
+  const long long nch = per_mat / chunk;
+  const uint8_t *b1 = reinterpret_cast<const uint8_t *>(a.bank_w1) + (size_t)s0 * a.F * a.d * 2;
+  const uint8_t *b3 = reinterpret_cast<const uint8_t *>(a.bank_w3) + (size_t)s0 * a.F * a.d * 2;
+  for (long long c = part; c < nch; c += nparts) {
+    prefetch_l2_bulk(b1 + c * chunk, (uint32_t)chunk);
+    prefetch_l2_bulk(b3 + c * chunk, (uint32_t)chunk);
+  }
+}
+
 __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallArgs a,
                                                   const __grid_constant__ RouteKeys rk) {
   extern __shared__ __align__(16) uint8_t fsm[];
@@ -438,26 +568,6 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
     *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
   int nbar = 0;
   TG_STAMP(0);
-  // ---- L2 prefetch of the weights the GEMM streams first.  The GEMM takes its
-  // GEMM1 units slot by slot; the first slot with rows is predicted from the
-  // previous call's per-slot counts (routing is sticky across decode steps).  A
-  // wrong guess only costs idle HBM bandwidth during this (latency-bound) kernel.
-  if (threadIdx.x == 0 && a.l2_prefetch_bytes > 0) {
-    int s0 = -1;
-    for (int s = 0; s < a.S_loc && s0 < 0; ++s)
-      if (__ldcg(a.slot_rows + s) > 0) s0 = s;
-    if (s0 >= 0) {
-      const long long per_mat = min((long long)a.F * a.d * 2, a.l2_prefetch_bytes / 2);  // W1 and W3 halves
-      const long long chunk = 65536;
-      const long long nch = per_mat / chunk;
-      const uint8_t *b1 = reinterpret_cast<const uint8_t *>(a.bank_w1) + (size_t)s0 * a.F * a.d * 2;
-      const uint8_t *b3 = reinterpret_cast<const uint8_t *>(a.bank_w3) + (size_t)s0 * a.F * a.d * 2;
-      for (long long c = blockIdx.x; c < nch; c += gridDim.x) {
-        prefetch_l2_bulk(b1 + c * chunk, (uint32_t)chunk);
-        prefetch_l2_bulk(b3 + c * chunk, (uint32_t)chunk);
-      }
-    }
-  }
   // ---- P1 router (+ reset of the GEMM counters of this call)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x < 4) a.sync[threadIdx.x] = 0;
@@ -472,38 +582,40 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
     R.part = reinterpret_cast<float *>(R.xt + kRouterRows * R.ldw);
     const int bpp = gridDim.x / nkp;  // blocks per K part
     const int kp = blockIdx.x % nkp, slot = blockIdx.x / nkp;
+    // chained (decode-sized calls): at most one router item per block, P1b-P3 run by
+    // the last arrivers; phased (prefill-sized): grid-stride phases between barriers,
+    // so no block serialises the top-k of many groups
+    const bool chain = ngroups <= bpp;
     if (slot < bpp && slot < ngroups) {
-      router_stage_wg(a, R, kp);
-      TG_STAMP(9);
       int it = 0;
       for (int grp = slot; grp < ngroups; grp += bpp, ++it) {
         if (it < 5) TG_STAMP(20 + 2 * it);
-        router_item(a, rk, R, grp, kp);
+        router_item(a, R, grp, kp, it == 0);
         if (it < 5) TG_STAMP(21 + 2 * it);
+        if (it == 0) l2_prefetch_share(a, blockIdx.x, min(bpp, ngroups) * nkp);
+        if (chain) group_arrive(a, rk, grp, nkp, ngroups, R.part);
       }
+    }
+    if (!chain) {
+      const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
+      grid_barrier_z(gbar, nbar++, a.err);
+      for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) group_topk(a, rk, grp, R.part);
+      TG_STAMP(12);
+      grid_barrier_z(gbar, nbar++, a.err);
+      for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, reinterpret_cast<uint8_t *>(R.part));
+      TG_STAMP(13);
+      grid_barrier_z(gbar, nbar++, a.err);
+      if (blockIdx.x == 0) {
+        TG_STAMP(1);
+        exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(R.part));
+        TG_STAMP(14);
+      }
+    } else if (ngroups == 0 && blockIdx.x == 0) {
+      // no tokens: the count exchange still runs (peers wait for this rank's counts)
+      exchange_counts(a, 0, reinterpret_cast<int32_t *>(R.part));
     }
   }
   if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + blockIdx.x] = globaltimer_ns();
-  grid_barrier_z(gbar, nbar++, a.err);
-  // ---- P1b top-k + softmax + ERT key, one warp per token over the whole grid
-  {
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    float *lrow = reinterpret_cast<float *>(fsm) + (threadIdx.x >> 5) * a.E_r;
-    for (int t = gw; t < a.T; t += nw) topk_warp(a, rk, t, lrow);
-  }
-  grid_barrier_z(gbar, nbar++, a.err);
-  TG_STAMP(1);
-  // ---- P2 rank (one chunk of 256 tokens per block)
-  const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
-  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, fsm);
-  // with a single chunk block 0 owns all ranks: P3 follows without a grid barrier
-  if (nchunks > 1) grid_barrier_z(gbar, nbar++, a.err);
-  TG_STAMP(2);
-  // ---- P3 counts exchange + layout (block 0)
-  if (blockIdx.x == 0) {
-    __syncthreads();
-    exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(fsm));
-  }
   grid_barrier_z(gbar, nbar++, a.err);
   TG_STAMP(3);
   // the GEMM kernel may launch now: its prologue overlaps the dispatch
@@ -555,11 +667,11 @@ __global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallAr
 
 static size_t front_smem(const CallArgs &a) {
   const int KP = router_kpart(a.d, a.E_r), ldw = KP / 2 + 4;
-  size_t r = sizeof(uint32_t) * (size_t)(router_epad(a.E_r) + kRouterRows) * ldw +
-             sizeof(float) * std::max(8 * kRouterRows * 64, kRouterRows * (a.E_r + 1));
-  size_t b = sizeof(uint32_t) * 8 * a.nkeys;
-  size_t e = sizeof(int32_t) * 3 * a.nkeys;
-  return std::max(r, std::max(b, e));
+  // R.wg + R.xt, then R.part: router warp partials, and in turn group top-k logits,
+  // the rank bitmap and the exchange arrays
+  const size_t topk = (size_t)kRouterRows * (a.E_r + 1) + kRouterRows * kMaxK;
+  const size_t part = std::max(std::max((size_t)8 * kRouterRows * 64, topk), (size_t)8 * a.nkeys);
+  return sizeof(uint32_t) * (size_t)(router_epad(a.E_r) + kRouterRows) * ldw + sizeof(float) * part;
 }
 
 cudaError_t launch_front(const CallArgs &a, const RouteKeys &rk, int n_sms, cudaStream_t s) {

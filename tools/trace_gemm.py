@@ -40,10 +40,17 @@ def main():
     tr = tg.tg_get_trace(layer.ctx)
     st = tr["front_stamps"]
     if st[0] > 0:
-        print("front kernel phase stamps (us from start: router, rank, exchange, dispatch):",
-              np.round((st[:5] - st[0]) / 1e3, 2).tolist())
-        t0g = tr["start"].min()
-        print("router detail (us from front start): zero-ctr %.2f wg-staged %.2f | item0: start %.2f x-tile %.2f mma+partials %.2f fence %.2f topk-start %.2f topk-end %.2f" % tuple((st[i] - st[0]) / 1e3 if st[i] else -1 for i in (8, 9, 10, 11, 12, 13, 14, 15)))
+        print("front kernel (us from start): group0 top-k %.2f, chunk0 rank %.2f, exchange start %.2f end %.2f, "
+              "grid barrier %.2f, dispatch done %.2f" % tuple((st[i] - st[0]) / 1e3 if st[i] else -1
+                                                             for i in (12, 13, 1, 14, 3, 4)))
+        print("group 0: part arrivals", [round((v - st[0]) / 1e3, 2) if v else -1 for v in st[40:48]],
+              "last-arriver start %.2f, logits summed %.2f, top-k done %.2f" % tuple((st[i] - st[0]) / 1e3 if st[i] else -1 for i in (30, 31, 12)))
+        print("row 0 top-k: entry %.2f select %.2f slots %.2f Z %.2f stores %.2f | pass1 done %.2f pass2 done %.2f" % tuple((st[i] - st[0]) / 1e3 if st[i] else -1 for i in (32, 33, 34, 35, 36, 37, 38)))
+        stc = tr["front_stamps_raw"]
+        if st[32] and st[33]:
+            print("row-0 select loop: %.2f us, %d SM cycles -> %.0f MHz" % ((st[33] - st[32]) / 1e3, stc[51] - stc[50], (stc[51] - stc[50]) / ((st[33] - st[32]) / 1e3)))
+        print("router detail (us from front start): zero-ctr %.2f | item0: start %.2f x-tile %.2f"
+              % tuple((st[i] - st[0]) / 1e3 if st[i] else -1 for i in (8, 10, 11)))
         print("block0 items (start,end) us:", [(round((st[20 + 2 * i] - st[0]) / 1e3, 2), round((st[21 + 2 * i] - st[0]) / 1e3, 2)) for i in range(5) if st[20 + 2 * i]])
         fb = (tr["front_block_p1"] - st[0]) / 1e3
         print("front P1 finish per block: min %.1f median %.1f max %.1f  argmax %d" % (fb.min(), np.median(fb), fb.max(), int(np.argmax(fb))))
