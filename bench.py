@@ -174,13 +174,18 @@ def make_weights_device(shape, seed, device, experts):
     return L
 
 
-def gemm_algorithmic_bytes(shape, slot_rows_active, R_local):
-    """GEMM kernel (GK4) algorithmic HBM bytes per launch:
-    weights of every slot with rows (3*d*F*2 each) + shared weights + token rows
-    read (R*d*2) + expert outputs written (R*d*2)."""
-    b = slot_rows_active * 3 * shape.d * shape.F * 2 + 2 * R_local * shape.d * 2
+def layer_algorithmic_bytes(shape, slot_rows_active, R_local, T_local):
+    """k_layer (the whole round trip, one launch) algorithmic HBM bytes per launch
+    on one rank: weights of every slot with rows (3*d*F*2 each) +
+    shared weights + router weights + tokens read (T*d*2) + dispatched rows
+    written and read (2*R*d*2) + expert outputs written (R*d*2) and read by the
+    combine (T*k*d*2) + outputs written (T*d*2)."""
+    d = shape.d
+    b = slot_rows_active * 3 * d * shape.F * 2
     if shape.F_sh:
-        b += 3 * shape.d * shape.F_sh * 2
+        b += 3 * d * shape.F_sh * 2
+    b += (shape.E + shape.shared_gate) * d * 2
+    b += T_local * d * 2 + 3 * R_local * d * 2 + T_local * shape.k * d * 2 + T_local * d * 2
     return b
 
 
@@ -350,15 +355,15 @@ def main():
     hbm, tf, tf_sus, src = peaks()
     names = tg.KERNEL_NAMES
     kt = dict(zip(names, ktimes))
-    g_ms = kt.get("gemm", float("nan"))
-    gbytes = gemm_algorithmic_bytes(shape, active, R_local)
+    g_ms = kt.get("layer", float("nan"))
+    gbytes = layer_algorithmic_bytes(shape, active, R_local, T_r)
     achieved = gbytes / (g_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(f"{cfg}:N{N}:T{T_glob}")
-    roof = {"bound": "hbm", "kernel": "k_gemm (GK4)", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+    roof = {"bound": "hbm", "kernel": "k_layer (front + dispatch || grouped FFN + combine, one launch)", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
             "algorithmic_bytes_per_launch": gbytes, "kernel_ms": g_ms,
             "kernel_share_of_step": (g_ms / (ms_prof / args.steps)) if ms_prof else None,

@@ -174,19 +174,19 @@ int tg_bank_slot(const tg_ctx *ctx, int ew, int slot);
  * rank's tokens: int64 [world][S_max] host array.  Synchronises the device. */
 tg_status tg_get_stats(tg_ctx *ctx, int64_t *rows);
 
-/* Per-kernel CUDA-event timing (events on the call's stream between launches,
- * no host synchronisation per call).  tg_set_profiling(ctx, 1) starts a new
- * record; tg_get_kernel_times(ctx, ms, &n) synchronises and writes n (= 2)
- * MEAN durations in ms over the recorded calls (at most the last 512), in
- * launch order: front (gate, rank, count exchange, dispatch) and gemm
- * (grouped expert FFN + fused combine exchange + combine).                 */
+/* Per-kernel CUDA-event timing (events on the call's stream around each
+ * launch, no host synchronisation per call).  tg_set_profiling(ctx, 1) starts
+ * a new record; tg_get_kernel_times(ctx, ms, &n) synchronises and writes n
+ * (= 1) MEAN durations in ms over the recorded calls (at most the last 512):
+ * the one launch of a call, k_layer (gate, rank, count exchange, dispatch ||
+ * grouped expert FFN, fused combine exchange, combine).                   */
 tg_status tg_set_profiling(tg_ctx *ctx, int on);
 tg_status tg_get_kernel_times(tg_ctx *ctx, float *ms, int *n);
 
-/* Diagnostics (performance analysis of the grouped GEMM kernel).
+/* Diagnostics (performance analysis of k_layer).
  * tg_set_trace(ctx, 1): subsequent calls record, per GEMM work unit, its
- * completion (globaltimer ns << 16 | unit kind << 12 | SM id), per CTA its
- * start time, and phase timestamps of the front kernel.
+ * completion (globaltimer ns << 16 | unit kind << 12 | SM id), per CTA the
+ * start time of its GEMM phase, and phase timestamps of the front phases.
  * tg_get_trace(ctx, trace, cap, &n_units, &n_ctas) synchronises and copies
  * the last call's records to the HOST array trace (uint64, cap entries):
  * [0, n_units) unit records, then 148 CTA start stamps, then 64 phase stamps. */

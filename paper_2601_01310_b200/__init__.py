@@ -253,7 +253,7 @@ def tg_finalize(ctx):
         _lib.tg_finalize(ctx)
 
 
-KERNEL_NAMES = ("front", "gemm")
+KERNEL_NAMES = ("layer",)
 
 
 # ----------------------------------------------------------------- convenience

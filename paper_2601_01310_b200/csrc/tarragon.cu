@@ -82,15 +82,14 @@ struct tg_ctx {
   bool tracing = false;
   int force_mode = -1;                           // TG_WIDE=0/1 (development A/B), -1 auto
   int force_dual = -1;                           // TG_G2DUAL=0/1 (development A/B), -1 auto
-  bool skip_gemm = false;                        // TG_SKIP_GEMM=1: front only (development timing, wrong outputs)
   bf16 *x_stage = nullptr, *out_stage = nullptr;   // for tg_moe_layer_host
   uint32_t epoch = 0;
   int last_T = 0;
   int last_launches = 0;
   bool sticky = false;
   // profiling
-  // profiling: 6 events per call, ring of kProfCalls calls, no host sync per call
-  static constexpr int kProfCalls = 512, kEv = 3;
+  // profiling: 2 events per call (around the one launch), ring of kProfCalls calls, no host sync per call
+  static constexpr int kProfCalls = 512, kEv = 2;
   bool prof = false;
   std::vector<cudaEvent_t> ev;
   int n_ev = 0;        // events recorded in the current call
@@ -204,6 +203,10 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   c->R_tot = c->R_cap + (Fsh > 0 ? c->T_max : 0);
   // fixed split-K for long GEMM2 reductions: a function of the shape only
   c->nsplit = (F / BK >= 128 && (F / BK) % 4 == 0) ? 4 : (F / BK >= 128 && (F / BK) % 2 == 0) ? 2 : 1;
+  if (const char *ns = getenv("TG_NSPLIT")) {  // development override (A/B timing)
+    const int v = atoi(ns);
+    if (v >= 1 && v <= 16 && (F / BK) % v == 0) c->nsplit = v;
+  }
   if (cuda_device < 0) { *out = c; return TG_OK; }
 
   // ---------------------------------------------------------------- device
@@ -307,8 +310,6 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
     if (wm && (wm[0] == '0' || wm[0] == '1')) c->force_mode = wm[0] - '0';
     const char *dm = getenv("TG_G2DUAL");
     if (dm && (dm[0] == '0' || dm[0] == '1')) c->force_dual = dm[0] - '0';
-    const char *sg = getenv("TG_SKIP_GEMM");
-    c->skip_gemm = sg && sg[0] == '1';
   }
   CKI(cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
   *c->err_host = 0;
@@ -336,7 +337,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
       c->maps.hs[i] = c->maps.h[i];
     }
   }
-  CKI(gemm_configure());
+  CKI(layer_configure());
   CKI(cudaDeviceSynchronize());
 #undef CKI
   *out = c;
@@ -546,24 +547,20 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
     bool wide = false;
     if (c->force_mode >= 0) wide = c->force_mode == 1;  // TG_WIDE development override
     a.bn = wide ? 256 : 128;
-    // prefill-sized calls (>= 192 rows per expert on average): GEMM2 units take two W2 tiles
-    const long long rows_avg = (long long)T * c->world * c->k / c->E;
-    a.g2dual = !wide && ((rows_avg >= 192 && c->force_dual != 0) || c->force_dual == 1);
-    a.nstages = wide ? 3 : 4;
-    a.stage_bytes = wide ? 65536 : 49152;
+    // GEMM2 units take two W2 tiles sharing one H tile: half the H bytes per W2 byte
+    // (the per-SM L2->SMEM stream, not HBM, is what the token tiles cost; r01 A/B: -5%)
+    a.g2dual = !wide && c->force_dual != 0;
   }
   a.trace = c->tracing ? c->trace : nullptr;
   a.alive = c->alive;
   for (int q = 0; q < kMaxWorld; ++q) a.sym[q] = q < c->world ? c->peer[q] : nullptr;
   c->n_ev = 0;
   rec(c, s);
-  CK(launch_front(a, rk, c->n_sms, s));
-  rec(c, s);
-  if (!c->skip_gemm) CK(launch_gemm(a, c->maps, c->n_sms, s));
+  CK(launch_layer(a, rk, c->maps, c->n_sms, s));
   rec(c, s);
   if (c->prof) ++c->prof_calls;
   c->last_T = T;
-  c->last_launches = 2;
+  c->last_launches = 1;
   return TG_OK;
 }
 

@@ -24,6 +24,7 @@
 //   w1  MMA issuer: one thread issues tcgen05.mma (bf16 -> fp32 in TMEM), two
 //       TMEM accumulator buffers so the epilogue overlaps the next unit.
 //   w2  TMEM allocator.   w3  slot plan.   w4-7  epilogue: tcgen05.ld -> global.
+#include "tg_front.cuh"
 #include "tg_internal.h"
 #include "tg_ptx.cuh"
 
@@ -41,6 +42,7 @@ struct GemmShared {
   int sched[kSchedDepth];
   uint32_t tmem_base;
   int red_last;
+  int nstages, stage_bytes;  // ring geometry of this call (build_plan)
   // slot plan of this call (routed slots, then the shared pseudo-slot)
   int NS, G1, total, ngroups;
   int nt[kMaxPlan];        // token tiles per slot
@@ -89,6 +91,10 @@ __device__ void build_plan(const CallArgs &a, GemmShared *P) {
     }
     return incl - v;
   };
+  // widest token tile of the call -> stage = one K block of two A tiles + that B tile
+  int nbw = 16;
+  for (int s = s0; s < s1; ++s) nbw = max(nbw, min(a.bn, (P->rows[s] + 15) / 16 * 16));
+  nbw = __reduce_max_sync(0xffffffffu, nbw);
   int br = xscan(sr), bu1 = xscan(su1), bu2 = xscan(su2), bg = xscan(sg), bred = xscan(sred);
   for (int s = s0; s < s1; ++s) {
     const bool sh = (s == S);
@@ -106,6 +112,8 @@ __device__ void build_plan(const CallArgs &a, GemmShared *P) {
     bred += (ns > 1) ? nt * ctiles : 0;
   }
   if (lane == 31) {
+    P->stage_bytes = 2 * kTileBytes + nbw * BK * 2;  // multiple of 2 KB: 1 KB swizzle-atom aligned
+    P->nstages = min(kStages, kRingBytes / P->stage_bytes);
     P->g1off[NS] = bu1;
     P->g2off[NS] = bu2;
     P->goff[NS] = bg;
@@ -186,13 +194,23 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
 }
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm(const __grid_constant__ TmaMaps maps, const __grid_constant__ CallArgs a) {
+    k_layer(const __grid_constant__ TmaMaps maps, const __grid_constant__ CallArgs a,
+            const __grid_constant__ RouteKeys rk) {
   extern __shared__ uint8_t smem_raw[];
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {  // launch gap: previous call's end -> this entry
+    a.trace[a.n_units_max + 148 + 19] = a.trace[a.n_units_max + 148 + 17];
+    a.trace[a.n_units_max + 148 + 18] = globaltimer_ns();
+  }
+  // PDL: everything below reads/writes state of the previous call's kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // ===================== front: P1 router .. P3 count exchange (tg_front.cuh) =====================
+  front_phase(a, rk, smem_raw);
+  // the ring below is refilled by TMA (async proxy) after the front's generic smem writes
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   // 1024-B aligned stage ring (128-B swizzle atoms), bookkeeping after it.
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t *ring = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
   GemmShared *S = reinterpret_cast<GemmShared *>(ring + kRingBytes);
-  const int nstages = a.nstages, stage_bytes = a.stage_bytes;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int *err = a.err;
@@ -214,14 +232,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tmem_alloc(&S->tmem_base, kTmemCols);
     tmem_relinquish();
   }
-  // PDL: the prologue above overlapped the front kernel; its outputs are read below
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 3) build_plan(a, S);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S->tmem_base;
   const int n_units = S->total;
+  const int nstages = S->nstages, stage_bytes = S->stage_bytes;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -229,16 +246,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_w1 = policy_evict_first();  // weight tiles streamed once (one token tile)
       const uint64_t pol_wn = policy_evict_last();   // weight tiles re-read by several token tiles
       const uint64_t pol_x = policy_evict_last();    // token tiles: re-read by every weight tile
-      // Dispatched rows from peers must have landed (release/acquire on
-      // per-source epoch flags), then order them before async-proxy reads.
-      for (int src = 0; src < a.world; ++src) {
-        if (__ldcg(a.need_src + src)) {
-          const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
-                               FLAG_DATA * kMaxWorld + src;
-          wait_flag_ge_s(fl, a.epoch, sys, err, 0x4001);
+      // Weight (A) tiles do not depend on the dispatch running on warps 2-7: the
+      // first ring stages get their A tiles at once and their token (B) tiles
+      // once the dispatched rows have landed (release/acquire on per-source
+      // epoch flags, then ordered before async-proxy reads).
+      bool data_ok = false;
+      int npend = 0;
+      int pst[kStages], pkb[kStages], pcnt[kStages], prow[kStages];
+      uint32_t pab[kStages], psub[kStages];
+      const CUtensorMap *pmap[kStages];
+      auto wait_data = [&]() {
+        for (int src = 0; src < a.world; ++src) {
+          if (__ldcg(a.need_src + src)) {
+            const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
+                                 FLAG_DATA * kMaxWorld + src;
+            wait_flag_ge_s(fl, a.epoch, sys, err, 0x4001);
+          }
         }
-      }
-      fence_proxy_async_global();
+        fence_proxy_async_global();
+        data_ok = true;
+        for (int i = 0; i < npend; ++i)
+          for (int j = 0; j < pcnt[i]; ++j)
+            tma_load_2d(ring + pst[i] * stage_bytes + j * psub[i] + pab[i], pmap[i], &S->full[pst[i]],
+                        (pkb[i] + j) * BK, prow[i], pol_x);
+        npend = 0;
+      };
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0;; ++it) {
@@ -248,11 +280,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&S->sempty[r], ((it / kSchedDepth) & 1) ^ 1, err);
         S->sched[r] = u;
         mbar_arrive(&S->sfull[r]);
-        if (u < 0) break;
+        if (u < 0) {
+          if (!data_ok && npend > 0) wait_data();
+          break;
+        }
         const Unit U = decode_unit(a, S, u);
         const bool g1 = (U.kind == U_G1 || U.kind == U_G1_SH);
         const bool sh = (U.kind == U_G1_SH || U.kind == U_G2_SH);
         if (!g1) {
+          if (!data_ok) wait_data();  // GEMM1 tiles waiting on pending B loads come first
           // all GEMM1 tiles of this (slot, n-tile) have written H
           wait_ctr_ge(a.ctr + U.dep, U.dep_target, err, 0x4002);
           fence_proxy_async_global();
@@ -271,6 +307,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint64_t pol_w = (U.ntiles > 1) ? pol_wn : pol_w1;
         for (int kb = U.kb0; kb < U.kb1; kb += kps) {
           const int cnt = min(kps, U.kb1 - kb);
+          if (!data_ok && npend == nstages) wait_data();  // every stage holds a pending B tile
           mbar_wait(&S->empty[stage], phase ^ 1, err);
           uint8_t *st = ring + stage * stage_bytes;
           mbar_arrive_expect_tx(&S->full[stage], (uint32_t)cnt * sub);
@@ -279,7 +316,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tma_load_2d(sb, mA0, &S->full[stage], (kb + i) * BK, rowA, pol_w);
             if (g1) tma_load_2d(sb + kTileBytes, mA1, &S->full[stage], (kb + i) * BK, rowA, pol_w);
             else if (U.dual) tma_load_2d(sb + kTileBytes, mA0, &S->full[stage], (kb + i) * BK, rowA + BM, pol_w);
-            tma_load_2d(sb + abytes, mB, &S->full[stage], (kb + i) * BK, rowB, pol_x);
+            if (data_ok) tma_load_2d(sb + abytes, mB, &S->full[stage], (kb + i) * BK, rowB, pol_x);
+          }
+          if (!data_ok) {
+            pst[npend] = stage; pkb[npend] = kb; pcnt[npend] = cnt; prow[npend] = rowB;
+            pab[npend] = abytes; psub[npend] = sub; pmap[npend] = mB;
+            ++npend;
           }
           if (++stage == nstages) { stage = 0; phase ^= 1; }
         }
@@ -325,8 +367,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t abytes = (two ? 2u : 1u) * kTileBytes;
         const uint32_t sub = abytes + (uint32_t)nb * BK * 2;
         const int kps = max(1, (int)(stage_bytes / sub));
-        for (int kb = U.kb0; kb < U.kb1; kb += kps) {
-          const int cnt = min(kps, U.kb1 - kb);
+        for (int j0 = 0; j0 < U.kb1 - U.kb0; j0 += kps) {
+          const int cnt = min(kps, U.kb1 - U.kb0 - j0);
           mbar_wait(&S->full[stage], phase, err);
           tc_fence_after();
           for (int i = 0; i < cnt; ++i) {
@@ -336,7 +378,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t dB = desc_sw128_kmajor(sa + abytes);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint32_t acc = (kb > U.kb0 || i > 0 || kk > 0) ? 1u : 0u;
+              const uint32_t acc = (j0 > 0 || i > 0 || kk > 0) ? 1u : 0u;
               // advance 16 K-elements = 32 B inside the swizzle row (>>4 units)
               umma_bf16_ss(d0, dA0 + 2 * kk, dB + 2 * kk, idesc, acc);
               if (two) umma_bf16_ss(d1, dA1 + 2 * kk, dB + 2 * kk, idesc, acc);
@@ -348,7 +390,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         umma_commit(&S->tfull[h]);
       }
     }
-  } else if (warp >= 4) {
+  } else {
+    // ===================== P4 dispatch (warps 2-7 of every CTA) =====================
+    dispatch_rows(a, blockIdx.x * 6 + (warp - 2), gridDim.x * 6);
+    named_bar_sync(2, 192);
+    if (threadIdx.x == 64) dispatch_done(a);
+  }
+  if (warp >= 4) {
     // ===================== epilogue (128 threads) =====================
     const int q = warp & 3;            // TMEM lane quarter of this warp
     const int et = threadIdx.x - 128;  // 0..127
@@ -577,15 +625,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 size_t gemm_smem_bytes() { return 1024 + (size_t)kRingBytes + sizeof(GemmShared); }
 
-cudaError_t gemm_configure() {
-  return cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes());
+static constexpr int kLayerSmemMax = 225 * 1024;  // + ~1 KB static smem: under the 227 KB opt-in
+static_assert(1024 + kRingBytes + sizeof(GemmShared) <= kLayerSmemMax, "GEMM smem over budget");
+
+cudaError_t layer_configure() {
+  return cudaFuncSetAttribute(k_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, kLayerSmemMax);
 }
 
-cudaError_t launch_gemm(const CallArgs &a, const TmaMaps &maps, int n_sms, cudaStream_t s) {
+size_t layer_smem_bytes(const CallArgs &a) { return tg_max(gemm_smem_bytes(), front_smem(a)); }
+
+cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_sms, cudaStream_t s) {
+  if (layer_smem_bytes(a) > (size_t)kLayerSmemMax) return cudaErrorInvalidConfiguration;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_sms);
   cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = gemm_smem_bytes();
+  cfg.dynamicSmemBytes = layer_smem_bytes(a);
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
@@ -594,7 +648,7 @@ cudaError_t launch_gemm(const CallArgs &a, const TmaMaps &maps, int n_sms, cudaS
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = a.pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k_gemm, maps, a);
+  return cudaLaunchKernelEx(&cfg, k_layer, maps, a, rk);
 }
 
 }  // namespace tg

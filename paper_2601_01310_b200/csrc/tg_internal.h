@@ -26,9 +26,9 @@ constexpr int kMaxSlotsPerRank = 256;
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int BN_MAX = 256;
-constexpr int kStages = 4;                      // maximum (narrow mode)
+constexpr int kStages = 8;                      // maximum ring depth (stage size set per call)
 constexpr int kTileBytes = 16384;               // 128 rows x 128 B
-constexpr int kRingBytes = 196608;              // 4 x 48 KB (narrow) or 3 x 64 KB (wide)
+constexpr int kRingBytes = 216 * 1024;          // stage ring: floor(216 KB / stage) stages
 constexpr int kSchedDepth = 8;
 constexpr int kGemmThreads = 256;               // w0 TMA, w1 MMA, w2 TMEM, w4-7 epilogue
 constexpr int kTmemCols = 512;                  // 2 accumulator buffers x 256 columns
@@ -88,7 +88,7 @@ struct CallArgs {
   int shared_gate;       // 1: shared expert scaled by sigmoid(x . wsg)
   int T;                 // tokens on this rank for this call
   uint32_t alive;        // bit r: rank r participates (fail-stopped ranks are never awaited or written)
-  int bn, nstages, stage_bytes;  // GEMM token-tile width and stage ring geometry of this call
+  int bn;                // GEMM token-tile width of this call (the stage ring geometry follows from the plan)
   int g2dual;            // GEMM2 units cover two 128-row W2 tiles sharing one H tile (prefill-sized calls)
   uint32_t epoch;
   // inputs / outputs
@@ -120,7 +120,7 @@ struct CallArgs {
   int32_t *n_units;      // [1] units of the last call (written by the GEMM, diagnostics)
   int n_units_max;       // capacity bound (trace sizing)
   int *err;              // host-mapped error word
-  int pdl;               // programmatic dependent launch between front and GEMM kernels
+  int pdl;               // programmatic dependent launch between consecutive calls
   uint64_t *trace;       // optional GEMM trace: [n_units_max] (end_ns << 16 | smid), [gridDim] start_ns
   // GEMM buffers (local)
   bf16 *H;               // [R_cap][F]
@@ -133,10 +133,11 @@ struct CallArgs {
 };
 
 // Kernel launchers (tg_kernels.cu / tg_gemm.cu).  Return cudaGetLastError().
-cudaError_t launch_front(const CallArgs &a, const RouteKeys &rk, int n_sms, cudaStream_t s);
-cudaError_t launch_gemm(const CallArgs &a, const TmaMaps &maps, int n_sms, cudaStream_t s);
+// the whole layer call: one cooperative launch of k_layer (front P1-P3, then
+// dispatch || grouped GEMM, combine)
+cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_sms, cudaStream_t s);
 cudaError_t launch_export_keys(const CallArgs &a, int n, int32_t *dst_rank, int32_t *dst_slot, cudaStream_t s);
-cudaError_t gemm_configure();
+cudaError_t layer_configure();
 size_t gemm_smem_bytes();
 
 }  // namespace tg

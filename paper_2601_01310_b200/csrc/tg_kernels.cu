@@ -1,700 +1,7 @@
-// tg_kernels.cu — GK1-3 "front" kernel of the MoE round trip (AW side, then the
-// dispatch exchange), one cooperative launch with grid barriers between phases:
-//
-//   P1 router   : router logits on tensor cores (bf16 x bf16 -> fp32), K split
-//                 in parts fixed by (d, E), partial logits to global memory
-//   P1b top-k   : one warp per token: parts summed in order, top-k (lowest id
-//                 on ties), softmax over the k selected, ERT resolve ->
-//                 destination key per pair
-//                 (§2.1; §4.2; §5.1).
-//   P2 rank     : stable rank of every (token, j) pair among this rank's pairs
-//                 with the same destination key, in token order (per-chunk
-//                 bitmaps + popcounts; §2.2.1 layer-wise batching).
-//   P3 exchange : (block 0) per-key totals, all-gather of per-source counts
-//                 with every peer over NVLink (one-sided stores + epoch
-//                 flag), receive layout on every destination.
-//   P4 dispatch : 16-B vector copies of token rows into the destination rank's
-//                 receive buffer (peer memory) + origin metadata, then a
-//                 per-source data-ready flag (§4.2).
-// The combine (GK5) runs at the end of the GEMM kernel (tg_gemm.cu).
-#include <algorithm>
-
+// tg_kernels.cu — small auxiliary kernels of libtarragon (parity exports).
 #include "tg_internal.h"
-#include "tg_ptx.cuh"
 
 namespace tg {
-
-
-#define TG_STAMP(i)                                                                     \
-  do {                                                                                  \
-    if (a.trace && threadIdx.x == 0 && blockIdx.x == 0)                                 \
-      a.trace[a.n_units_max + 148 + (i)] = globaltimer_ns();                            \
-  } while (0)
-
-#define TG_STAMP_ANY(i)                                                                 \
-  do {                                                                                  \
-    if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + (i)] = globaltimer_ns(); \
-  } while (0)
-
-// --------------------------------------------------------------------- P1
-// Router logits on tensor cores.  The K dimension is cut into parts of KP
-// elements (a function of d and E only); block b owns part kp = b % nkp for
-// the whole phase and stages the Wg slice [E][KP] in shared memory once (rows
-// padded by 16 B: conflict-free fragment loads).  Work item = (32-token group,
-// part): the x tile [32][KP] is staged with coalesced 16-B loads, warp w
-// reduces KP/8 elements with mma.sync.m16n8k16 (bf16 in, fp32 accumulate;
-// bf16 products are exact), k16 steps in order, the 8 warp partials are summed
-// in warp order and written to global memory; the last part of a group to
-// arrive sums the parts in part order and runs the top-k.  The reduction tree
-// of a logit depends only on (d, E) — never on T, the token's group or its row
-// — so routing is deterministic and row-invariant.
-constexpr int kRouterRows = 32;
-
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__host__ __device__ __forceinline__ int router_kpart(int d, int E) {
-  int kp = E <= 96 ? 512 : (E <= 192 ? 256 : 128);
-  while (kp > 64 && d % kp) kp >>= 1;  // d % 64 == 0, so 64 always divides d
-  return kp;
-}
-__host__ __device__ __forceinline__ int router_nkp(int d, int E) { return (d + router_kpart(d, E) - 1) / router_kpart(d, E); }
-__host__ __device__ __forceinline__ int router_epad(int E) { return (E + 63) / 64 * 64; }
-
-
-struct RouterSmem {
-  uint32_t *wg;   // [Epad][KP/2 + 4] words
-  uint32_t *xt;   // [32][KP/2 + 4] words
-  float *part;    // [8][32][64]
-  int ldw;        // row stride in words
-};
-
-// Batched copy of rows of 16-B chunks into padded smem rows: 16 loads in flight per
-// thread before the stores (these loops are latency-bound, not bandwidth-bound).
-template <typename RowPtr, typename DstRow>
-__device__ __forceinline__ void stage_rows(int nrows, int cpr, RowPtr row, DstRow drow) {
-  const int total = nrows * cpr;
-  const int lc = __ffs(cpr) - 1;  // cpr = KP / 8 is a power of two
-#pragma unroll 1
-  for (int i0 = threadIdx.x; i0 < total; i0 += 16 * blockDim.x) {
-    uint4 v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u * blockDim.x;
-      const uint4 *p = (i < total) ? row(i >> lc) : nullptr;
-      v[u] = p ? __ldg(p + (i & (cpr - 1))) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i < total) *reinterpret_cast<uint4 *>(drow(i >> lc) + (i & (cpr - 1)) * 4) = v[u];
-    }
-  }
-}
-
-__device__ void router_item(const CallArgs &a, const RouterSmem &R, int grp, int kp, bool with_wg) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = a.d, E = a.E_r, T = a.T;  // router rows: experts (+ shared-gate row)
-  const int g = lane >> 2, c = lane & 3;
-  const int KP = router_kpart(d, E), nkp = router_nkp(d, E), Epad = router_epad(E);
-  const int t0 = grp * kRouterRows;
-  const int cpr = KP / 8;
-  if (grp == 0 && kp == 0) TG_STAMP(10);
-  // x tile [32][KP] -> smem (rows past T clamped; their results are never used); on the
-  // block's first item the Wg slice [E8][KP] joins the same load batch (one latency)
-  const int E8 = with_wg ? (E + 7) / 8 * 8 : 0;  // Wg rows of the n8 tiles actually used
-  stage_rows(
-      E8 + kRouterRows, cpr,
-      [&](int r) -> const uint4 * {
-        if (r < E8) return r < E ? reinterpret_cast<const uint4 *>(a.wg + (size_t)r * d + kp * KP) : nullptr;
-        return reinterpret_cast<const uint4 *>(a.x + (size_t)min(t0 + r - E8, T - 1) * d + kp * KP);
-      },
-      [&](int r) -> uint32_t * { return (r < E8 ? R.wg + r * R.ldw : R.xt + (r - E8) * R.ldw); });
-  __syncthreads();
-  if (grp == 0 && kp == 0) TG_STAMP(11);
-  const int ksw = max(16, KP / 8);   // K elements of this warp (multiple of 16)
-  const int nsteps = (warp * ksw < KP) ? ksw / 16 : 0;
-  const int wk0 = warp * ksw / 2;    // first word column
-  float *dst = a.logit_part + ((size_t)grp * nkp + kp) * kRouterRows * E;
-  for (int e0 = 0; e0 < Epad; e0 += 64) {
-    const int ntr = min(8, (E - e0 + 7) / 8);  // n8 tiles holding real experts
-    float acc[2][8][4];
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int n = 0; n < 8; ++n)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[m][n][i] = 0.f;
-    for (int s = 0; s < nsteps; ++s) {
-      const int wc = wk0 + 8 * s + c;  // word column of k = 16 s + 2 c
-      uint32_t af[2][4];
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const uint32_t *x0 = R.xt + (16 * m + g) * R.ldw, *x1 = x0 + 8 * R.ldw;
-        af[m][0] = x0[wc];
-        af[m][1] = x1[wc];
-        af[m][2] = x0[wc + 4];
-        af[m][3] = x1[wc + 4];
-      }
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        if (n < ntr) {
-          const uint32_t *wr = R.wg + (e0 + 8 * n + g) * R.ldw;
-          const uint32_t b0 = wr[wc], b1 = wr[wc + 4];
-          mma_bf16_16816(acc[0][n], af[0], b0, b1);
-          mma_bf16_16816(acc[1][n], af[1], b0, b1);
-        }
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        if (n >= ntr) continue;
-        float *p = R.part + (warp * kRouterRows + 16 * m) * 64 + 8 * n + 2 * c;
-        p[g * 64] = acc[m][n][0];
-        p[g * 64 + 1] = acc[m][n][1];
-        p[(g + 8) * 64] = acc[m][n][2];
-        p[(g + 8) * 64 + 1] = acc[m][n][3];
-      }
-    __syncthreads();
-    const int ew = min(64, E - e0);
-    for (int i = threadIdx.x; i < kRouterRows * ew; i += blockDim.x) {
-      const int r = i / ew, ee = i % ew, e = e0 + ee;
-      {
-        const int pi = r * 64 + ee;
-        float sum = R.part[pi];
-#pragma unroll
-        for (int ww = 1; ww < 8; ++ww) sum += R.part[ww * kRouterRows * 64 + pi];
-        dst[r * E + e] = sum;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// --------------------------------------------------------------------- P2
-// Chunk of 256 tokens: bit t of bm[K][t/32] is set iff
-// token t has a pair with key K (at most one per token: its k experts are
-// distinct and map to distinct slots); the rank of (t, K) in the chunk is the
-// popcount of the bits below t.
-// One warp per token (P1b, all blocks): logits = sum of the K parts in part
-// order (lanes own experts lane + 32 i), staged in a warp-private smem row.
-// Expert e is selected iff fewer than k experts beat it, where e' beats e iff
-// l[e'] > l[e] or (l[e'] == l[e] and e' < e) (lowest id wins ties; -0 == +0
-// compare equal).  Its slot is the number of selected experts with a smaller id
-// (slots in ascending expert id, R#4).  Softmax over the k selected:
-// m = max, z_j = expf(l_j - m), Z = ((z_0 + z_1) + ...) in slot order,
-// w_j = z_j / Z (IEEE).
-// P1b for one 32-token group, by the block that delivered its last K part (or by
-// a grid-stride loop in phased mode).  Logits = sum of the parts in part order
-// (16 loads in flight per thread) into smem rows.  Top-k: 8 lanes per token (one
-// warp holds 4 tokens), k rounds of a warp arg-max under the strict total order
-// "(v, e) beats (v', e') iff v > v' or (v == v' and e < e')" — lowest id wins
-// ties, -0 == +0; NaN logits read as -inf — so round j picks the expert beaten
-// by exactly j others and the picks are {e : fewer than k experts beat e}.
-// Slots in ascending expert id (R#4); softmax over the k selected with m = top-1
-// logit, z_j = expf(l_j - m), Z = ((z_0 + z_1) + ...) in slot order (gate_mode
-// 0), or over all E as 8 per-lane ascending partial sums combined by a fixed xor
-// tree (gate_mode 1); w_j = z_j / Z (IEEE).  Every reduction order depends on
-// (E, k) only: deterministic and row-invariant.  (Latency matters here, not
-// work: short dependency chains, no branches in the scans.)
-__device__ __forceinline__ bool beats(float v, int e, float v2, int e2) {
-  return (v > v2) | ((v == v2) & (e < e2));
-}
-
-
-// Top-k of one token on 8 lanes (sub = lane & 7 holds experts e = sub + 8 i,
-// i < PER, in registers): k rounds of arg-max (local chain, then a 3-level xor
-// tree within the 8 lanes); the owner marks its pick taken.  Lane j keeps the
-// j-th pick.
-template <int PER>
-__device__ __forceinline__ void topk_rows(const CallArgs &a, const RouteKeys &rk, int t0, bool act,
-                                          const float *l, int *rsl) {
-  const int E = a.E, k = a.k, lane = threadIdx.x & 31, sub = lane & 7;
-  const int r = threadIdx.x >> 3;
-  float v[PER];
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int e = sub + 8 * i;
-    float x = (act && e < E) ? l[e] : -INFINITY;
-    v[i] = (x != x) ? -INFINITY : x;
-  }
-  uint32_t taken = 0;
-  int mine = 0x7fffffff;
-  float mval = 0.f, m = 0.f;
-#pragma unroll 1
-  for (int j = 0; j < k; ++j) {
-    float bv = -INFINITY;
-    int be = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int e = sub + 8 * i;
-      const bool ok = (e < E) & !((taken >> i) & 1u) & beats(v[i], e, bv, be);
-      bv = ok ? v[i] : bv;
-      be = ok ? e : be;
-    }
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-      const bool tk = beats(ov, oe, bv, be);
-      bv = tk ? ov : bv;
-      be = tk ? oe : be;
-    }
-    if ((be & 7) == sub) taken |= 1u << (be >> 3);
-    if (sub == j) { mine = be; mval = bv; }
-    if (j == 0) m = bv;  // top-1 logit = max of the selected
-  }
-  // slot = picks with a smaller id (ascending expert id, R#4)
-  int slot = 0;
-#pragma unroll 1
-  for (int jj = 0; jj < k; ++jj) slot += __shfl_sync(0xffffffffu, mine, (lane & ~7) + jj) < mine;
-  if (sub < k) rsl[slot] = mine;
-  __syncwarp();
-  float Z = 0.f;
-  if (a.gate_mode == 0) {
-#pragma unroll 1
-    for (int s = 0; act && s < k; ++s) {  // fixed slot order
-      const float zs = expf(l[rsl[s]] - m);
-      Z = (s == 0) ? zs : Z + zs;
-    }
-  } else {
-    // softmax over all E: per-lane partial sums in ascending i, then a fixed xor tree
-#pragma unroll
-    for (int i = 0; i < PER; ++i)
-      if (sub + 8 * i < E) Z += expf(v[i] - m);
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
-  }
-  if (act) {
-    const int t = t0 + r;
-    if (sub < k) {
-      const size_t o = (size_t)t * k + slot;
-      a.idx[o] = mine;
-      a.w[o] = __fdiv_rn(expf(mval - m), Z);
-      a.key[o] = rk.key[mine];
-    }
-    if (a.shared_gate && sub == 0) a.sgate[t] = __fdiv_rn(1.0f, 1.0f + expf(-l[E]));  // router row E
-  }
-}
-
-__device__ __forceinline__ void group_topk(const CallArgs &a, const RouteKeys &rk, int grp, float *sm) {
-  const int Er = a.E_r, E = a.E, nkp = router_nkp(a.d, Er), ld = Er + 1;  // padded rows
-  const int t0 = grp * kRouterRows, nrow = min(kRouterRows, a.T - t0);
-  const int n = nrow * Er;
-  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * Er;
-  float *lsum = sm;                                              // [32][Er + 1]
-  int *sl = reinterpret_cast<int *>(lsum + kRouterRows * ld);    // [32][kMaxK] selected ids by slot
-  const int bd = blockDim.x;
-#pragma unroll 1
-  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * bd) {
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-    for (int q0 = 0; q0 < nkp; q0 += 4) {
-      float p[4][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          p[u][q] = (i0 + u * bd < n && q0 + q < nkp)
-                        ? __ldcg(src + (size_t)(q0 + q) * kRouterRows * Er + i0 + u * bd) : 0.f;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q0 + q < nkp) s[u] = (q0 + q == 0) ? p[u][q] : s[u] + p[u][q];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * bd;
-      if (i < n) lsum[i + i / Er] = s[u];  // row i / Er, padded stride Er + 1
-    }
-  }
-  __syncthreads();
-  if (grp == 0) TG_STAMP_ANY(31);
-  // 256 threads = 32 tokens x 8; all lanes run every step (shuffles), writes are predicated
-  const int r = threadIdx.x >> 3;
-  const int per = (E + 7) / 8;
-  if (per <= 1) topk_rows<1>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else if (per <= 2) topk_rows<2>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else if (per <= 4) topk_rows<4>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else if (per <= 8) topk_rows<8>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else if (per <= 16) topk_rows<16>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else topk_rows<32>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  if (grp == 0) TG_STAMP_ANY(37);
-  __syncthreads();
-  __syncthreads();
-}
-
-__device__ __forceinline__ void rank_chunk(const CallArgs &a, int chunk, uint8_t *smraw) {
-  const int tid = threadIdx.x, nkeys = a.nkeys, k = a.k;
-  uint32_t *bm = reinterpret_cast<uint32_t *>(smraw);  // [nkeys][8]
-  const int t = chunk * kRankBlock + tid;
-  for (int i = tid; i < nkeys * 8; i += blockDim.x) bm[i] = 0;
-  __syncthreads();
-  int K[kMaxK];
-  for (int j = 0; j < k; ++j) {
-    K[j] = (t < a.T) ? __ldcg(a.key + (size_t)t * k + j) : -1;
-    if (K[j] >= 0) atomicOr(&bm[K[j] * 8 + (tid >> 5)], 1u << (tid & 31));
-  }
-  __syncthreads();
-  for (int j = 0; j < k; ++j) {
-    if (K[j] < 0) continue;
-    const uint32_t *row = bm + K[j] * 8;
-    int r = __popc(row[tid >> 5] & ((1u << (tid & 31)) - 1u));
-    for (int wd = 0; wd < (tid >> 5); ++wd) r += __popc(row[wd]);
-    a.lrank[(size_t)t * k + j] = r;
-  }
-  for (int Kk = tid; Kk < nkeys; Kk += blockDim.x) {
-    int c = 0;
-#pragma unroll
-    for (int wd = 0; wd < 8; ++wd) c += __popc(bm[Kk * 8 + wd]);
-    a.bcnt[(size_t)chunk * nkeys + Kk] = c;
-  }
-  __syncthreads();
-}
-
-// --------------------------------------------------------------------- P3
-__device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
-  const int tid = threadIdx.x, nkeys = a.nkeys;
-  int32_t *tot = sm;              // [nkeys] this rank's rows per key
-  int32_t *gsum = sm + nkeys;     // [nkeys] rows per key over all sources
-  int32_t *below = gsum + nkeys;  // [nkeys] rows per key from lower sources
-  const int par = a.epoch & 1;
-  const bool sys = a.world > 1;
-  for (int K = tid; K < nkeys; K += blockDim.x) {
-    int run = 0;
-    for (int b0 = 0; b0 < nchunks; b0 += 8) {  // 8 loads in flight
-      int c[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = (b0 + u < nchunks) ? __ldcg(a.bcnt + (size_t)(b0 + u) * nkeys + K) : 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (b0 + u < nchunks) {
-          a.bcnt[(size_t)(b0 + u) * nkeys + K] = run;  // exclusive chunk base
-          run += c[u];
-        }
-    }
-    tot[K] = run;
-    atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + K), (unsigned long long)run);
-  }
-  __syncthreads();
-  if (a.world == 1) {
-    // no peers: the gathered counts are this rank's own
-    for (int K = tid; K < nkeys; K += blockDim.x) {
-      gsum[K] = tot[K];
-      below[K] = 0;
-      a.gcounts[K] = tot[K];
-    }
-    __syncthreads();
-    for (int K = tid; K < nkeys; K += blockDim.x) {
-      const int s = K % a.S_max;
-      int off = 0;
-      for (int s2 = 0; s2 < s; ++s2) off += gsum[s2];
-      a.dbase[K] = off;
-    }
-    if (tid == 0) {
-      int any = 0;
-      for (int K = 0; K < nkeys; ++K) any |= tot[K];
-      a.need_src[0] = any > 0;
-      a.sent_to[0] = any > 0;
-    }
-    for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[s];
-    return;
-  }
-  // all-gather: my totals -> cnt_all[par][rank][*] on every live peer, then release flags
-  for (int q = 0; q < a.world; ++q) {
-    if (!((a.alive >> q) & 1u)) continue;
-    int32_t *dst = reinterpret_cast<int32_t *>(a.sym[q] + a.L.cnt_all) + ((size_t)par * a.world + a.rank) * nkeys;
-    for (int K = tid; K < nkeys; K += blockDim.x) dst[K] = tot[K];
-  }
-  __syncthreads();
-  if (tid < a.world && ((a.alive >> tid) & 1u)) {
-    fence_scope(sys);
-    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[tid] + a.L.flags) + FLAG_CNT * kMaxWorld + a.rank;
-    st_release(fl, a.epoch, sys);
-    const uint32_t *mine = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + FLAG_CNT * kMaxWorld + tid;
-    wait_flag_ge_s(mine, a.epoch, sys, a.err, 0x2001);
-  }
-  __syncthreads();
-  const int32_t *A = reinterpret_cast<const int32_t *>(a.sym[a.rank] + a.L.cnt_all) + (size_t)par * a.world * nkeys;
-  for (int K = tid; K < nkeys; K += blockDim.x) {
-    int g = 0, bl = 0;
-    for (int src = 0; src < a.world; ++src) {
-      const int c = ((a.alive >> src) & 1u) ? __ldcg(A + (size_t)src * nkeys + K) : 0;  // dead: no rows
-      if (src < a.rank) bl += c;
-      g += c;
-    }
-    gsum[K] = g;
-    below[K] = bl;
-    a.gcounts[K] = g;
-  }
-  __syncthreads();
-  // dbase[K] = rows of lower slots on that rank (all sources) + rows of lower sources
-  for (int K = tid; K < nkeys; K += blockDim.x) {
-    const int q = K / a.S_max, s = K % a.S_max;
-    int off = 0;
-    for (int s2 = 0; s2 < s; ++s2) off += gsum[q * a.S_max + s2];
-    a.dbase[K] = off + below[K];
-  }
-  if (tid < a.world) {
-    int to_me = 0, to_q = 0;
-    for (int s = 0; s < a.S_max; ++s) {
-      to_me += ((a.alive >> tid) & 1u) ? __ldcg(A + (size_t)tid * nkeys + a.rank * a.S_max + s) : 0;
-      to_q += tot[tid * a.S_max + s];
-    }
-    a.need_src[tid] = to_me > 0;
-    a.sent_to[tid] = to_q > 0;
-  }
-  for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[a.rank * a.S_max + s];
-}
-
-// ------------------------------------------------------- P1 -> P3 chaining
-// No grid barriers between P1, P1b, P2 and P3: the block that delivers the last
-// K part of a 32-token group runs its top-k (P1b); the block that completes the
-// last group of a 256-token chunk ranks the chunk (P2); the block that completes
-// the last chunk runs the count exchange (P3).  Arrival = __threadfence + atomic
-// counter (threadfence-reduction pattern); the last arriver resets the counter
-// for the next call (kernel boundaries order the calls).
-__device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, int nkp, int ngroups, float *sm) {
-  __shared__ int s_last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const int last = atomicAdd(a.grp_ctr + grp, 1) == nkp - 1;
-    if (last) {
-      a.grp_ctr[grp] = 0;
-      __threadfence();
-    }
-    s_last = last;
-  }
-  __syncthreads();
-  if (grp == 0 && a.trace && threadIdx.x == 0)
-    a.trace[a.n_units_max + 148 + 40 + (blockIdx.x % nkp)] = globaltimer_ns();  // arrival of each part
-  if (!s_last) return;
-  if (grp == 0) TG_STAMP_ANY(30);
-  group_topk(a, rk, grp, sm);
-  if (grp == 0) TG_STAMP_ANY(12);
-  constexpr int gpc = kRankBlock / kRouterRows;
-  const int ch = grp / gpc, nchunks = (a.T + kRankBlock - 1) / kRankBlock;
-  const int ng_ch = min(gpc, ngroups - ch * gpc);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const int last = atomicAdd(a.chunk_ctr + 1 + ch, 1) == ng_ch - 1;
-    if (last) {
-      a.chunk_ctr[1 + ch] = 0;
-      __threadfence();
-    }
-    s_last = last;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  rank_chunk(a, ch, reinterpret_cast<uint8_t *>(sm));
-  if (ch == 0) TG_STAMP_ANY(13);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const int last = atomicAdd(a.chunk_ctr, 1) == nchunks - 1;
-    if (last) {
-      a.chunk_ctr[0] = 0;
-      __threadfence();
-    }
-    s_last = last;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  TG_STAMP_ANY(1);
-  exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(sm));
-  TG_STAMP_ANY(14);
-  __syncthreads();
-}
-
-// --------------------------------------------------------------------- P4
-// Warp copy of one row of nch 16-B chunks: up to 16 loads of a lane in flight
-// before its stores (the copy is latency-bound per warp).
-__device__ __forceinline__ void copy_row(uint4 *__restrict__ dst, const uint4 *__restrict__ src, int nch, int lane) {
-  for (int c0 = lane; c0 < nch; c0 += 16 * 32) {
-    uint4 v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int c = c0 + 32 * u;
-      if (c < nch) v[u] = __ldg(src + c);
-    }
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int c = c0 + 32 * u;
-      if (c < nch) dst[c] = v[u];
-    }
-  }
-}
-
-// L2 prefetch of the weights the GEMM streams first (block `part` of `nparts`
-// issues its share).  The GEMM takes its GEMM1 units slot by slot; the first
-// slot with rows is predicted from the previous call's per-slot counts (routing
-// is sticky across decode steps).  A wrong guess only costs idle HBM bandwidth
-// during this latency-bound kernel.  Issued after the router's own loads so the
-// HBM queues serve those first.
-__device__ void l2_prefetch_share(const CallArgs &a, int part, int nparts) {
-  // issued by warp 1: thread 0's __threadfence in the arrival must not wait for these
-  if (threadIdx.x != 32 || a.l2_prefetch_bytes <= 0) return;
-  int s0 = -1;
-  for (int s = 0; s < a.S_loc && s0 < 0; ++s)
-    if (__ldcg(a.slot_rows + s) > 0) s0 = s;
-  if (s0 < 0) return;
-  const long long per_mat = min((long long)a.F * a.d * 2, a.l2_prefetch_bytes / 2);  // W1 and W3 halves
-  const long long chunk = 65536;
-  const long long nch = per_mat / chunk;
-  const uint8_t *b1 = reinterpret_cast<const uint8_t *>(a.bank_w1) + (size_t)s0 * a.F * a.d * 2;
-  const uint8_t *b3 = reinterpret_cast<const uint8_t *>(a.bank_w3) + (size_t)s0 * a.F * a.d * 2;
-  for (long long c = part; c < nch; c += nparts) {
-    prefetch_l2_bulk(b1 + c * chunk, (uint32_t)chunk);
-    prefetch_l2_bulk(b3 + c * chunk, (uint32_t)chunk);
-  }
-}
-
-__global__ void __launch_bounds__(256, 1) k_front(const __grid_constant__ CallArgs a,
-                                                  const __grid_constant__ RouteKeys rk) {
-  extern __shared__ __align__(16) uint8_t fsm[];
-  // grid barriers of this call count on sync[8 + 4 * (epoch & 1)] (u64) from 0; the other
-  // counter is reset here for the next call (the previous call has completed: PDL wait below)
-  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
-  // PDL: everything below reads/writes state of the previous call's GEMM kernel
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
-  int nbar = 0;
-  TG_STAMP(0);
-  // ---- P1 router (+ reset of the GEMM counters of this call)
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x < 4) a.sync[threadIdx.x] = 0;
-  TG_STAMP(8);
-  const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
-  {
-    const int nkp = router_nkp(a.d, a.E_r), KP = router_kpart(a.d, a.E_r), Epad = router_epad(a.E_r);
-    RouterSmem R;
-    R.ldw = KP / 2 + 4;
-    R.wg = reinterpret_cast<uint32_t *>(fsm);
-    R.xt = R.wg + Epad * R.ldw;
-    R.part = reinterpret_cast<float *>(R.xt + kRouterRows * R.ldw);
-    const int bpp = gridDim.x / nkp;  // blocks per K part
-    const int kp = blockIdx.x % nkp, slot = blockIdx.x / nkp;
-    // chained (decode-sized calls): at most one router item per block, P1b-P3 run by
-    // the last arrivers; phased (prefill-sized): grid-stride phases between barriers,
-    // so no block serialises the top-k of many groups
-    const bool chain = ngroups <= bpp;
-    if (slot < bpp && slot < ngroups) {
-      int it = 0;
-      for (int grp = slot; grp < ngroups; grp += bpp, ++it) {
-        if (it < 5) TG_STAMP(20 + 2 * it);
-        router_item(a, R, grp, kp, it == 0);
-        if (it < 5) TG_STAMP(21 + 2 * it);
-        if (it == 0) l2_prefetch_share(a, blockIdx.x, min(bpp, ngroups) * nkp);
-        if (chain) group_arrive(a, rk, grp, nkp, ngroups, R.part);
-      }
-    }
-    if (!chain) {
-      const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
-      grid_barrier_z(gbar, nbar++, a.err);
-      for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) group_topk(a, rk, grp, R.part);
-      TG_STAMP(12);
-      grid_barrier_z(gbar, nbar++, a.err);
-      for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, reinterpret_cast<uint8_t *>(R.part));
-      TG_STAMP(13);
-      grid_barrier_z(gbar, nbar++, a.err);
-      if (blockIdx.x == 0) {
-        TG_STAMP(1);
-        exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(R.part));
-        TG_STAMP(14);
-      }
-    } else if (ngroups == 0 && blockIdx.x == 0) {
-      // no tokens: the count exchange still runs (peers wait for this rank's counts)
-      exchange_counts(a, 0, reinterpret_cast<int32_t *>(R.part));
-    }
-  }
-  if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + blockIdx.x] = globaltimer_ns();
-  grid_barrier_z(gbar, nbar++, a.err);
-  TG_STAMP(3);
-  // the GEMM kernel may launch now: its prologue overlaps the dispatch
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // ---- P4 dispatch: one warp per (token, j) pair
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int k = a.k, nch = a.d >> 3;
-  const int npairs = a.T * k;
-  const int nsh = (a.Fsh > 0) ? a.T : 0;
-  for (int p = warp; p < npairs + nsh; p += nwarps) {
-    if (p < npairs) {
-      const int t = p / k;
-      const int K = __ldcg(a.key + p);
-      const int q = K / a.S_max;
-      const int pos =
-          __ldcg(a.dbase + K) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K) + __ldcg(a.lrank + p);
-      const uint4 *src = reinterpret_cast<const uint4 *>(a.x + (size_t)t * a.d);
-      uint4 *dst = reinterpret_cast<uint4 *>(a.sym[q] + a.L.recv) + (size_t)pos * nch;
-      copy_row(dst, src, nch, lane);
-      if (lane == 0) {
-        int2 *meta = reinterpret_cast<int2 *>(a.sym[q] + a.L.meta);
-        meta[pos] = make_int2(a.rank, p);
-        a.dst_pos[p] = pos;
-      }
-    } else {
-      const int t = p - npairs;
-      const uint4 *src = reinterpret_cast<const uint4 *>(a.x + (size_t)t * a.d);
-      uint4 *dst = reinterpret_cast<uint4 *>(a.sym[a.rank] + a.L.recv) + (size_t)(a.R_sh0 + t) * nch;
-      copy_row(dst, src, nch, lane);
-    }
-  }
-  // data-ready flags: the last block to finish releases one flag per destination
-  const bool sys = a.world > 1;
-  __shared__ int s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_scope(sys);
-    s_last = (atomicAdd(&a.sync[3], 1) == (int)gridDim.x - 1);
-  }
-  __syncthreads();
-  if (s_last && threadIdx.x < a.world && ((a.alive >> threadIdx.x) & 1u)) {
-    fence_scope(sys);
-    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[threadIdx.x] + a.L.flags) + FLAG_DATA * kMaxWorld + a.rank;
-    st_release(fl, a.epoch, sys);
-  }
-  TG_STAMP(4);
-}
-
-static size_t front_smem(const CallArgs &a) {
-  const int KP = router_kpart(a.d, a.E_r), ldw = KP / 2 + 4;
-  // R.wg + R.xt, then R.part: router warp partials, and in turn group top-k logits,
-  // the rank bitmap and the exchange arrays
-  const size_t topk = (size_t)kRouterRows * (a.E_r + 1) + kRouterRows * kMaxK;
-  const size_t part = std::max(std::max((size_t)8 * kRouterRows * 64, topk), (size_t)8 * a.nkeys);
-  return sizeof(uint32_t) * (size_t)(router_epad(a.E_r) + kRouterRows) * ldw + sizeof(float) * part;
-}
-
-cudaError_t launch_front(const CallArgs &a, const RouteKeys &rk, int n_sms, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_sms);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = front_smem(a);
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = a.pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, k_front, a, rk);
-}
 
 // Parity export: destination key -> (rank, bank slot) of every pair of the last call.
 __global__ void k_export_keys(const int32_t *key, int n, int S_max, int32_t *dr, int32_t *ds) {

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="mixtral_decode")
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--W", type=int, default=1)
+    ap.add_argument("--warm", type=int, default=5, help="untraced calls first (1000+: power-capped steady state)")
     a = ap.parse_args()
     sh = wl.CONFIGS[a.config]
     T = a.tokens or sh.T
@@ -32,10 +33,11 @@ def main():
     L = make_weights_device(sh, 1001, dev, list(range(sh.E)))
     layer = tg.MoELayer(sh, pl, L, max_tokens_per_rank=T, device=0)
     x = wl.make_tokens(sh, 1001, T=T, device=dev)
-    for _ in range(5):
+    for _ in range(a.warm):
         layer(x)
     tg.tg_set_trace(layer.ctx, True)
     layer(x)
+    layer(x)  # second traced call: the first one's end stamp gives the launch gap
     torch.cuda.synchronize()
     tr = tg.tg_get_trace(layer.ctx)
     st = tr["front_stamps"]
@@ -56,6 +58,10 @@ def main():
         print("front P1 finish per block: min %.1f median %.1f max %.1f  argmax %d" % (fb.min(), np.median(fb), fb.max(), int(np.argmax(fb))))
         tc = tr["topk_cycles"]
         print("per-block gather/topk kcycles (cumulative over traced calls): max gather %.1f max topk %.1f, block of max topk %d" % (tc[:, 0].max() / 1e3, tc[:, 1].max() / 1e3, int(np.argmax(tc[:, 1]))))
+        if st[19] and st[18]:
+            print("launch gap: previous call end -> entry %.2f us, entry -> front start (PDL wait) %.2f us"
+                  % ((st[18] - st[19]) / 1e3, (st[0] - st[18]) / 1e3))
+        t0g = tr["start"].min()
         print("gemm: CTA start %.1f us after front start; grid barrier at %.1f, combine done %.1f us after GEMM start"
               % ((t0g - st[0]) / 1e3, (st[16] - t0g) / 1e3, (st[17] - t0g) / 1e3))
     np.savez(os.path.join(ROOT, "gpurun_out", f"trace_{a.config}_{T}.npz"), **tr)
