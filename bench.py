@@ -376,7 +376,7 @@ def main():
         Lh = wl.Layer(shape, L.wg.cpu(), [w.cpu() for w in L.w1], [w.cpu() for w in L.w3],
                       [w.cpu() for w in L.w2], tuple(w.cpu() for w in L.shared) if L.shared else None,
                       L.wsg.cpu() if L.wsg is not None else None)
-        xc = xs[0].cpu()
+        xc = torch.cat([b.cpu() for b in xs])  # up to NB batches: a sample of ~12 s of CPU work
         v, dt = cpu_oracle_sample(shape, Lh, xc, pl, n, cores)
         if args.cpu_sample is None and dt < 8.0:
             # scale the sample to ~12 s of CPU work (bounded by the batch)
