@@ -145,6 +145,34 @@ tg_status tg_mask_worker(tg_ctx *ctx, int ew, int masked);
  * masked = 0 on a masked rank returns TG_ERR_UNSUPPORTED.  Host-only.      */
 tg_status tg_mask_rank(tg_ctx *ctx, int rank, int masked);
 
+/* In-call EW failover (§5.1 "the AW re-dispatches the affected
+ * tokens to a shadow").  During a call, this rank's waits on a
+ * PEER's data-ready and combine flags give up after the failure timeout
+ * (default 200 ms; tg_set_failure_timeout, (0, 4000] ms) and record the peer as
+ * failed instead of trapping; the call completes with the outputs of the pairs
+ * that peer held undefined.  tg_failover(ctx, x, out, n_tokens, stream, &failed)
+ * then synchronises `stream` and, if the last tg_moe_layer saw a failure:
+ * fail-stops the failed ranks (as tg_mask_rank), re-routes the pairs this rank
+ * had sent them to the next live candidate of each expert (ERT order) and
+ * recomputes them and `out` for every token, all within the same call's inputs
+ * (x, n_tokens must be the failed call's; outputs of pairs other EWs served are
+ * kept) — bitwise the output an unfailed call gives.  *failed = bit mask of the
+ * failed ranks (0: nothing to do, out untouched).  Returns TG_OK, or
+ * TG_ERR_NO_ROUTE when some re-routed pair's next live candidate is on another
+ * rank (not recomputed in this call; the mask is applied for the next call).
+ * Scope: fail-stop peers that failed after the count exchange of the call (a
+ * peer that never publishes its counts stalls the exchange: device error, as
+ * before); other survivors must also mask the failed rank before their next
+ * call (tg_failover or tg_mask_rank).                                       */
+tg_status tg_set_failure_timeout(tg_ctx *ctx, double ms);
+tg_status tg_failover(tg_ctx *ctx, const void *x, void *out, int n_tokens, void *stream, uint32_t *failed);
+
+/* Fault injection (tests): the next tg_moe_layer on this ctx runs its front
+ * and dispatch and then stops, as a process that crashes mid-call (peers hold
+ * its rows and wait for its expert outputs).  The ctx is dead afterwards:
+ * only tg_finalize may follow.                                               */
+tg_status tg_inject_failure(tg_ctx *ctx);
+
 /* One MoE layer round trip (collective: every live rank calls it, same order).
  * x: device bf16 [n_tokens][d] (this rank's tokens); out: device bf16
  * [n_tokens][d], must not alias x.  n_tokens <= max_tokens_per_rank (may be

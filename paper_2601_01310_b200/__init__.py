@@ -54,6 +54,9 @@ _SIG = {
     "tg_set_route_table": ([_P, _U64, _P, _I], _I),
     "tg_mask_worker": ([_P, _I, _I], _I),
     "tg_mask_rank": ([_P, _I, _I], _I),
+    "tg_set_failure_timeout": ([_P, ctypes.c_double], _I),
+    "tg_failover": ([_P, _P, _P, _I, _P, ctypes.POINTER(ctypes.c_uint32)], _I),
+    "tg_inject_failure": ([_P], _I),
     "tg_moe_layer": ([_P, _P, _P, _I, _P], _I),
     "tg_moe_layer_host": ([_P, _P, _P, _I, _P], _I),
     "tg_get_routing": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
@@ -173,6 +176,23 @@ def tg_mask_rank(ctx, rank: int, masked: int = 1) -> int:
     """Fail-stop a whole rank (AW + its EWs); returns TG_OK or TG_ERR_NO_ROUTE (warning)."""
     rc = _lib.tg_mask_rank(ctx, rank, masked)
     return _check(ctx, rc, "tg_mask_rank", ok=(TG_OK, TG_ERR_NO_ROUTE))
+
+
+def tg_set_failure_timeout(ctx, ms: float) -> int:
+    return _check(ctx, _lib.tg_set_failure_timeout(ctx, float(ms)), "tg_set_failure_timeout")
+
+
+def tg_inject_failure(ctx) -> int:
+    return _check(ctx, _lib.tg_inject_failure(ctx), "tg_inject_failure")
+
+
+def tg_failover(ctx, x: torch.Tensor, out: torch.Tensor, stream=None):
+    """In-call failover after a tg_moe_layer: returns (status, failed rank mask)."""
+    f = ctypes.c_uint32(0)
+    rc = _lib.tg_failover(ctx, _ptr(x), _ptr(out), x.shape[0] if x is not None else 0, _stream(stream),
+                          ctypes.byref(f))
+    _check(ctx, rc, "tg_failover", ok=(TG_OK, TG_ERR_NO_ROUTE))
+    return rc, int(f.value)
 
 
 def tg_moe_layer(ctx, x: torch.Tensor, out: torch.Tensor, stream=None) -> int:
@@ -317,6 +337,10 @@ class MoELayer:
 
     def mask_rank(self, rank, masked=1):
         return tg_mask_rank(self.ctx, rank, masked)
+
+    def failover(self, x: torch.Tensor, out: torch.Tensor, stream=None):
+        """After a call: repair `out` if an EW failed mid-call; returns (status, failed rank mask)."""
+        return tg_failover(self.ctx, x, out, stream)
 
     def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         if out is None:

@@ -83,7 +83,11 @@ struct tg_ctx {
   int force_mode = -1;                           // TG_WIDE=0/1 (development A/B), -1 auto
   int force_dual = -1;                           // TG_G2DUAL=0/1 (development A/B), -1 auto
   bf16 *x_stage = nullptr, *out_stage = nullptr;   // for tg_moe_layer_host
-  uint32_t epoch = 0;
+  uint32_t epoch = 0;    // local kernel runs
+  uint32_t xepoch = 0;   // calls (equal on every rank)
+  int32_t *key_main = nullptr, *key_replay = nullptr;
+  long long fail_timeout_ns = 200000000LL;  // in-call failure detection on data / combine flags
+  bool inject_next = false;                 // fault injection for tests (tg_inject_failure)
   int last_T = 0;
   int last_launches = 0;
   bool sticky = false;
@@ -248,7 +252,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   L.meta = off; off = align_up(off + (size_t)c->R_tot * 8, 1024);
   L.ybuf = off; off = align_up(off + Tm * k * d * 2, 1024);
   L.cnt_all = off; off = align_up(off + (size_t)2 * world * c->nkeys * 4, 1024);
-  L.flags = off; off = align_up(off + 3 * kMaxWorld * 4, 1024);
+  L.flags = off; off = align_up(off + kNumFlagKinds * kMaxWorld * 4, 1024);
   L.total = off;
   CKI(cudaMalloc(&c->sym, L.total));
   CKI(cudaMemset(c->sym, 0, L.total));
@@ -265,6 +269,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   auto carve = [&](size_t bytes) { size_t o = so; so = align_up(so + bytes, 256); return o; };
   size_t o_sg = carve(Tm * 4);
   size_t o_idx = carve(Tm * k * 4), o_w = carve(Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
+  size_t o_key2 = carve(Tm * k * 4);
   size_t o_lp = carve(((Tm + 31) / 32) * (size_t)(d / 64) * 32 * (E + 1) * 4);  // groups * nkp * 32 * E floats (KP >= 64)
   size_t o_gc2 = carve(((Tm + 31) / 32) * 4), o_cc = carve((size_t)(1 + nblk_max) * 4);
   size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
@@ -294,6 +299,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   }
   a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.sgate = (float *)(sb + o_sg);
   a.gate_mode = c->gate_mode; a.shared_gate = c->shared_gate; a.E_r = E + c->shared_gate; a.key = (int32_t *)(sb + o_key);
+  c->key_main = a.key; c->key_replay = (int32_t *)(sb + o_key2);
   a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.chunk_ctr = (int32_t *)(sb + o_cc); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
   a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
   a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
@@ -315,6 +321,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   *c->err_host = 0;
   CKI(cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
   a.err = c->err_dev;
+  a.fail_mask = reinterpret_cast<uint32_t *>(c->err_dev + 4);  // host-mapped words [4], [5]
+  a.unrec = c->err_dev + 5;
   // tensor maps (fixed addresses)
   tg_status s;
   if ((s = make_map(c, &c->maps.w1, c->bank_w1, S_loc * F, d, BM)) != TG_OK) return bail(s);
@@ -514,6 +522,38 @@ static void rec(tg_ctx *c, cudaStream_t s) {
   if (c->n_ev < tg_ctx::kEv) cudaEventRecord(c->ev[(size_t)slot * tg_ctx::kEv + c->n_ev++], s);
 }
 
+// Per-call kernel arguments (everything but the epochs of the flags).
+static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys *rk) {
+  for (int e = 0; e < kMaxExperts; ++e) rk->key[e] = e < c->E ? c->rkey[e] : -1;
+  CallArgs a = c->args;
+  a.T = T;
+  a.x = reinterpret_cast<const bf16 *>(x);
+  a.out = reinterpret_cast<bf16 *>(out);
+  a.epoch = ++c->epoch;
+  {
+    // Wide token tiles (bn = 256) cut the L2 bytes per FLOP of prefill tiles but
+    // measured slower on B200 (per-SM L2->SMEM delivery, not bytes/FLOP, limits
+    // them; profiles/README.md r01): narrow by default, wide on request.
+    bool wide = false;
+    if (c->force_mode >= 0) wide = c->force_mode == 1;  // TG_WIDE development override
+    a.bn = wide ? 256 : 128;
+    // GEMM2 units take two W2 tiles sharing one H tile: half the H bytes per W2 byte
+    // (the per-SM L2->SMEM stream, not HBM, is what the token tiles cost; r01 A/B: -5%)
+    a.g2dual = !wide && c->force_dual != 0;
+  }
+  a.trace = c->tracing ? c->trace : nullptr;
+  a.alive = c->alive;
+  a.fslot_data = FLAG_DATA;
+  a.fslot_comb = FLAG_COMB;
+  a.fail_timeout_ns = c->fail_timeout_ns;
+  a.replay = 0;
+  a.failed = 0;
+  a.key_old = nullptr;
+  a.inject_fail = 0;
+  for (int q = 0; q < kMaxWorld; ++q) a.sym[q] = q < c->world ? c->peer[q] : nullptr;
+  return a;
+}
+
 tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream) {
   if (!c) return TG_ERR_INVALID;
   if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device): no compute path");
@@ -534,26 +574,11 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(c->device));
   RouteKeys rk;
-  for (int e = 0; e < kMaxExperts; ++e) rk.key[e] = e < c->E ? c->rkey[e] : -1;
-  CallArgs a = c->args;
-  a.T = T;
-  a.x = reinterpret_cast<const bf16 *>(x);
-  a.out = reinterpret_cast<bf16 *>(out);
-  a.epoch = ++c->epoch;
-  {
-    // Wide token tiles (bn = 256) cut the L2 bytes per FLOP of prefill tiles but
-    // measured slower on B200 (per-SM L2->SMEM delivery, not bytes/FLOP, limits
-    // them; profiles/README.md r01): narrow by default, wide on request.
-    bool wide = false;
-    if (c->force_mode >= 0) wide = c->force_mode == 1;  // TG_WIDE development override
-    a.bn = wide ? 256 : 128;
-    // GEMM2 units take two W2 tiles sharing one H tile: half the H bytes per W2 byte
-    // (the per-SM L2->SMEM stream, not HBM, is what the token tiles cost; r01 A/B: -5%)
-    a.g2dual = !wide && c->force_dual != 0;
-  }
-  a.trace = c->tracing ? c->trace : nullptr;
-  a.alive = c->alive;
-  for (int q = 0; q < kMaxWorld; ++q) a.sym[q] = q < c->world ? c->peer[q] : nullptr;
+  CallArgs a = call_args(c, T, x, out, &rk);
+  a.xepoch = ++c->xepoch;
+  a.fepoch = a.xepoch;
+  a.inject_fail = c->inject_next ? 1 : 0;
+  c->inject_next = false;
   c->n_ev = 0;
   rec(c, s);
   CK(launch_layer(a, rk, c->maps, c->n_sms, s));
@@ -561,6 +586,65 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   if (c->prof) ++c->prof_calls;
   c->last_T = T;
   c->last_launches = 1;
+  return TG_OK;
+}
+
+tg_status tg_set_failure_timeout(tg_ctx *c, double ms) {
+  if (!c) return TG_ERR_INVALID;
+  if (!(ms > 0.0) || ms > 4000.0) return fail(c, TG_ERR_INVALID, "failure timeout %g ms not in (0, 4000]", ms);
+  c->fail_timeout_ns = (long long)(ms * 1e6);
+  return TG_OK;
+}
+
+tg_status tg_inject_failure(tg_ctx *c) {
+  if (!c) return TG_ERR_INVALID;
+  c->inject_next = true;
+  return TG_OK;
+}
+
+tg_status tg_failover(tg_ctx *c, const void *x, void *out, int T, void *stream, uint32_t *failed) {
+  if (!c) return TG_ERR_INVALID;
+  if (failed) *failed = 0;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device): no compute path");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(s));
+  tg_status st = check_sticky(c);
+  if (st) return st;
+  volatile int *hw = reinterpret_cast<volatile int *>(c->err_host);
+  const uint32_t fm = static_cast<uint32_t>(hw[4]) & ~(1u << c->rank);
+  if (!fm) return TG_OK;  // the last call saw no peer failure: nothing to do
+  if (T != c->last_T) return fail(c, TG_ERR_INVALID, "failover needs the failed call's tokens (%d, got %d)", c->last_T, T);
+  hw[4] = 0;
+  hw[5] = 0;
+  // the failed ranks are fail-stopped from now on (as tg_mask_rank) ...
+  for (int q = 0; q < c->world; ++q)
+    if ((fm >> q) & 1u) {
+      c->alive &= ~(1u << q);
+      for (int w = 0; w < c->W; ++w)
+        if (c->ew_rank[w] == q) c->mask[w] = 1;
+    }
+  resolve(c);
+  if (failed) *failed = fm;
+  // ... and the pairs this rank sent them are recomputed on the next live candidate
+  RouteKeys rk;
+  CallArgs a = call_args(c, T, x, out, &rk);
+  a.xepoch = c->xepoch;
+  a.fepoch = a.epoch;
+  a.fslot_data = FLAG_RDATA;
+  a.fslot_comb = FLAG_RCOMB;
+  a.alive = 1u << c->rank;  // local by construction: no peer takes part
+  a.replay = 1;
+  a.failed = fm;
+  a.key_old = c->key_main;
+  a.key = c->key_replay;
+  CK(launch_layer(a, rk, c->maps, c->n_sms, s));
+  CK(cudaStreamSynchronize(s));
+  st = check_sticky(c);
+  if (st) return st;
+  if (hw[5] > 0)
+    return fail(c, TG_ERR_NO_ROUTE, "%d pairs have their next live candidate on another rank: not recomputed "
+                "in this call (their tokens' outputs are incomplete)", hw[5]);
   return TG_OK;
 }
 

@@ -368,7 +368,7 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
   int32_t *tot = sm;              // [nkeys] this rank's rows per key
   int32_t *gsum = sm + nkeys;     // [nkeys] rows per key over all sources
   int32_t *below = gsum + nkeys;  // [nkeys] rows per key from lower sources
-  const int par = a.epoch & 1;
+  const int par = a.xepoch & 1;
   const bool sys = a.world > 1;
   for (int K = tid; K < nkeys; K += blockDim.x) {
     int run = 0;
@@ -387,8 +387,10 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
     atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + K), (unsigned long long)run);
   }
   __syncthreads();
-  if (a.world == 1) {
-    // no peers: the gathered counts are this rank's own
+  if (a.world == 1 || a.replay) {
+    // no peers (or a failover replay, local by construction): the gathered counts are this
+    // rank's own, and only its own keys carry rows
+    const int k0 = a.rank * a.S_max;
     for (int K = tid; K < nkeys; K += blockDim.x) {
       gsum[K] = tot[K];
       below[K] = 0;
@@ -396,18 +398,20 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
     }
     __syncthreads();
     for (int K = tid; K < nkeys; K += blockDim.x) {
-      const int s = K % a.S_max;
+      const int s = K - k0;
       int off = 0;
-      for (int s2 = 0; s2 < s; ++s2) off += gsum[s2];
+      if (s >= 0 && s < a.S_max)
+        for (int s2 = 0; s2 < s; ++s2) off += gsum[k0 + s2];
       a.dbase[K] = off;
     }
-    if (tid == 0) {
+    if (tid < a.world) {
       int any = 0;
-      for (int K = 0; K < nkeys; ++K) any |= tot[K];
-      a.need_src[0] = any > 0;
-      a.sent_to[0] = any > 0;
+      if (tid == a.rank)
+        for (int s = 0; s < a.S_max; ++s) any |= tot[k0 + s];
+      a.need_src[tid] = any > 0;
+      a.sent_to[tid] = any > 0;
     }
-    for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[s];
+    for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[k0 + s];
     return;
   }
   // all-gather: my totals -> cnt_all[par][rank][*] on every live peer, then release flags
@@ -420,9 +424,9 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
   if (tid < a.world && ((a.alive >> tid) & 1u)) {
     fence_scope(sys);
     uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[tid] + a.L.flags) + FLAG_CNT * kMaxWorld + a.rank;
-    st_release(fl, a.epoch, sys);
+    st_release(fl, a.xepoch, sys);
     const uint32_t *mine = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + FLAG_CNT * kMaxWorld + tid;
-    wait_flag_ge_s(mine, a.epoch, sys, a.err, 0x2001);
+    wait_flag_ge_s(mine, a.xepoch, sys, a.err, 0x2001);
   }
   __syncthreads();
   const int32_t *A = reinterpret_cast<const int32_t *>(a.sym[a.rank] + a.L.cnt_all) + (size_t)par * a.world * nkeys;
@@ -622,6 +626,39 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   TG_STAMP(3);
 }
 
+// In-call failover (NEXT-1, §5.1): replay of the last
+// call's pairs whose destination rank failed.  Every such pair takes the next live
+// candidate of its expert (rk = the resolution after masking the failed ranks),
+// which must be a shadow on this rank; the others keep their (good) outputs.  Then
+// P2 and a local P3 (no peer takes part) as in a normal call.
+__device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys &rk, uint8_t *fsm) {
+  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 4) a.sync[threadIdx.x] = 0;
+  int nbar = 0;
+  const int npairs = a.T * a.k;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
+    const int K = __ldcg(a.key_old + p);
+    int nk = -1;
+    if (K >= 0 && ((a.failed >> (K / a.S_max)) & 1u)) {
+      nk = rk.key[__ldcg(a.idx + p)];
+      if (nk < 0 || nk / a.S_max != a.rank) {  // next candidate on another rank: not in this call
+        atomicAdd(a.unrec, 1);
+        nk = -1;
+      }
+    }
+    a.key[p] = nk;
+  }
+  grid_barrier_z(gbar, nbar++, a.err);
+  const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, fsm);
+  grid_barrier_z(gbar, nbar++, a.err);
+  if (blockIdx.x == 0) exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(fsm));
+  grid_barrier_z(gbar, nbar++, a.err);
+}
+
 // P4 dispatch on `nw` warps (this one is warp `w`, grid-wide numbering): one warp
 // per (token, j) pair, then the shared-expert rows.  The caller syncs its
 // dispatch warps and calls dispatch_done() from one thread.
@@ -629,11 +666,12 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) 
   const int lane = threadIdx.x & 31;
   const int k = a.k, nch = a.d >> 3;
   const int npairs = a.T * k;
-  const int nsh = (a.Fsh > 0) ? a.T : 0;
+  const int nsh = (a.Fsh > 0 && !a.replay) ? a.T : 0;  // a replay keeps the shared expert's output
   for (int p = w; p < npairs + nsh; p += nw) {
     if (p < npairs) {
       const int t = p / k;
       const int K = __ldcg(a.key + p);
+      if (K < 0) continue;  // failover replay: pair not recomputed
       const int q = K / a.S_max;
       const int pos =
           __ldcg(a.dbase + K) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K) + __ldcg(a.lrank + p);
@@ -663,8 +701,8 @@ __device__ __forceinline__ void dispatch_done(const CallArgs &a) {
   fence_scope(sys);
   for (int q = 0; q < a.world; ++q) {
     if (!((a.alive >> q) & 1u)) continue;
-    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[q] + a.L.flags) + FLAG_DATA * kMaxWorld + a.rank;
-    st_release(fl, a.epoch, sys);
+    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[q] + a.L.flags) + a.fslot_data * kMaxWorld + a.rank;
+    st_release(fl, a.fepoch, sys);
   }
   if (a.trace) a.trace[a.n_units_max + 148 + 4] = globaltimer_ns();
 }

@@ -63,7 +63,7 @@ __device__ __forceinline__ int box_index(int nrows) { return ((nrows + 15) >> 4)
 // Warp-parallel exclusive scan of per-slot quantities (lanes own contiguous slot ranges).
 __device__ void build_plan(const CallArgs &a, GemmShared *P) {
   const int lane = threadIdx.x & 31;
-  const int S = a.S_loc, nsh = a.Fsh > 0 ? 1 : 0, NS = S + nsh;
+  const int S = a.S_loc, nsh = (a.Fsh > 0 && !a.replay) ? 1 : 0, NS = S + nsh;
   const int ftiles = (a.F + BM - 1) / BM, ctiles = (a.d + BM * (a.g2dual ? 2 : 1) - 1) / (BM * (a.g2dual ? 2 : 1));
   const int ftiles_sh = nsh ? (a.Fsh + BM - 1) / BM : 0;
   const int per = (NS + 31) / 32;
@@ -204,7 +204,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // PDL: everything below reads/writes state of the previous call's kernel
   asm volatile("griddepcontrol.wait;" ::: "memory");
   // ===================== front: P1 router .. P3 count exchange (tg_front.cuh) =====================
-  front_phase(a, rk, smem_raw);
+  if (a.replay) replay_front(a, rk, smem_raw);
+  else front_phase(a, rk, smem_raw);
+  if (a.inject_fail) {  // fault injection (tests): crash after the dispatch, the peers hold the rows
+    dispatch_rows(a, blockIdx.x * 8 + (threadIdx.x >> 5), gridDim.x * 8);
+    __syncthreads();
+    if (threadIdx.x == 0) dispatch_done(a);
+    return;
+  }
   // the ring below is refilled by TMA (async proxy) after the front's generic smem writes
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   // 1024-B aligned stage ring (128-B swizzle atoms), bookkeeping after it.
@@ -259,8 +266,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int src = 0; src < a.world; ++src) {
           if (__ldcg(a.need_src + src)) {
             const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
-                                 FLAG_DATA * kMaxWorld + src;
-            wait_flag_ge_s(fl, a.epoch, sys, err, 0x4001);
+                                 a.fslot_data * kMaxWorld + src;
+            if (src == a.rank) {
+              wait_flag_ge_s(fl, a.fepoch, sys, err, 0x4001);
+            } else if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) {
+              atomicOr(a.fail_mask, 1u << src);  // its rows never landed: computed on stale data, discarded
+            }
           }
         }
         fence_proxy_async_global();
@@ -566,13 +577,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (blockIdx.x == 0 && threadIdx.x < a.world && ((a.alive >> threadIdx.x) & 1u)) {
     // every expert output this rank computed is in its source's combine buffer
     fence_scope(sys);
-    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[threadIdx.x] + a.L.flags) + FLAG_COMB * kMaxWorld + a.rank;
-    st_release(fl, a.epoch, sys);
+    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[threadIdx.x] + a.L.flags) + a.fslot_comb * kMaxWorld + a.rank;
+    st_release(fl, a.fepoch, sys);
   }
-  if (threadIdx.x < a.world && __ldcg(a.sent_to + threadIdx.x)) {
+  if (threadIdx.x < a.world && ((a.alive >> threadIdx.x) & 1u) && __ldcg(a.sent_to + threadIdx.x)) {
     const uint32_t *fl =
-        reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + FLAG_COMB * kMaxWorld + threadIdx.x;
-    wait_flag_ge_s(fl, a.epoch, sys, err, 0x5001);
+        reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + a.fslot_comb * kMaxWorld + threadIdx.x;
+    if (threadIdx.x == a.rank) {
+      wait_flag_ge_s(fl, a.fepoch, sys, err, 0x5001);
+    } else if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) {
+      // an EW that took rows from this rank failed mid-call: its pairs are recomputed by
+      // tg_failover on the shadows (in-call failover, §5.1)
+      atomicOr(a.fail_mask, 1u << threadIdx.x);
+    }
   }
   __syncthreads();
   const int nch = a.d >> 3;

@@ -74,10 +74,10 @@ struct SymLayout {
   size_t meta;      // int2 [R_cap]               origin (src rank, t*k + j)
   size_t ybuf;      // bf16 [T_max][k][d]         expert outputs returned to this AW
   size_t cnt_all;   // int32 [2][world][nkeys]    all-gathered per-source counts
-  size_t flags;     // uint32 [3][kMaxWorld]      cnt / data / comb epoch flags
+  size_t flags;     // uint32 [5][kMaxWorld]      cnt / data / comb epoch flags, replay data / comb
   size_t total;
 };
-constexpr int FLAG_CNT = 0, FLAG_DATA = 1, FLAG_COMB = 2;
+constexpr int FLAG_CNT = 0, FLAG_DATA = 1, FLAG_COMB = 2, FLAG_RDATA = 3, FLAG_RCOMB = 4, kNumFlagKinds = 5;
 
 // Everything a call needs, by value (kernel parameter).
 struct CallArgs {
@@ -90,7 +90,18 @@ struct CallArgs {
   uint32_t alive;        // bit r: rank r participates (fail-stopped ranks are never awaited or written)
   int bn;                // GEMM token-tile width of this call (the stage ring geometry follows from the plan)
   int g2dual;            // GEMM2 units cover two 128-row W2 tiles sharing one H tile (prefill-sized calls)
-  uint32_t epoch;
+  uint32_t epoch;        // local kernel-run counter (grid barriers)
+  uint32_t xepoch;       // cross-rank call counter (count flags, count parity): equal on every rank
+  uint32_t fepoch;       // value of this run's data / combine flags (xepoch, or epoch for a replay)
+  int fslot_data, fslot_comb;  // flag kinds of this run (FLAG_DATA/COMB, or FLAG_RDATA/RCOMB)
+  // in-call failover (NEXT-1, §5.1)
+  long long fail_timeout_ns;   // data / combine waits on peers: timeout -> peer failed (not a trap)
+  uint32_t *fail_mask;         // host-mapped: bit q = peer q failed during a call
+  int *unrec;                  // host-mapped: replayed pairs whose next route is not on this rank
+  int replay;            // 1: recompute pairs routed to failed ranks (key_old) on this rank's shadows
+  uint32_t failed;       // replay: ranks whose pairs are recomputed
+  const int32_t *key_old;  // replay: the failed call's destination keys
+  int inject_fail;       // fault injection (tests): stop after the dispatch, as a crash mid-call
   // inputs / outputs
   const bf16 *x;
   bf16 *out;

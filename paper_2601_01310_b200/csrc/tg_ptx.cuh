@@ -201,6 +201,17 @@ __device__ __forceinline__ void wait_flag_ge_s(const uint32_t *flag, uint32_t ep
   }
 }
 
+// Wait on a PEER's flag with failure detection: false if it did not reach epoch
+// within timeout_ns (the peer is taken as failed; no trap).
+__device__ __forceinline__ bool wait_flag_or_fail(const uint32_t *flag, uint32_t epoch, bool sys, long long timeout_ns) {
+  if (static_cast<int32_t>(ld_acquire(flag, sys) - epoch) >= 0) return true;
+  uint64_t t0 = globaltimer_ns();
+  while (static_cast<int32_t>(ld_acquire(flag, sys) - epoch) < 0) {
+    if ((long long)(globaltimer_ns() - t0) > timeout_ns) return false;
+  }
+  return true;
+}
+
 // Spin until *flag >= epoch (wrap-safe), bounded.
 __device__ __forceinline__ void wait_flag_ge(const uint32_t *flag, uint32_t epoch, int *err, int code) {
   if (static_cast<int32_t>(ld_acquire_sys(flag) - epoch) >= 0) return;

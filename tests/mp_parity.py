@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--sample", type=int, default=0, help="oracle FFN on this many sampled tokens (0 = all)")
     ap.add_argument("--rank-fail", action="store_true",
                     help="fail-stop the last rank (tg_mask_rank) instead of the EW/flip checks")
+    ap.add_argument("--inflight-fail", action="store_true",
+                    help="the last rank crashes mid-call; survivors repair that call (tg_failover)")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -98,6 +100,10 @@ def main():
         msgs.append(f"rank {rank}: run-to-run differs")
     if a.rank_fail:
         ok = rank_fail_checks(a, tg, layer, pl, sh, W, rank, world, dev, out, run, msgs, rep) and ok
+        finish(ok, rank, rep, msgs, layer, dev)
+        return
+    if a.inflight_fail:
+        ok = inflight_fail_checks(tg, layer, rank, world, out, run, xr, msgs, rep) and ok
         finish(ok, rank, rep, msgs, layer, dev)
         return
     # mask EW1 (+ poison its slots on its rank) -> bit-identical
@@ -181,6 +187,53 @@ def rank_fail_checks(a, tg, layer, pl, sh, W, rank, world, dev, out, run, msgs, 
         rep["rank_fail_calls"] = 6
     rep["rank_fail_dead"] = dead
     # the failed process is still alive for the harness: it meets the survivors only here
+    dist.barrier()
+    return ok
+
+
+def inflight_fail_checks(tg, layer, rank, world, out, run, xr, msgs, rep):
+    """NEXT-1 (§5.1): the last rank crashes in the middle of a call (after its count
+    exchange and dispatch, before its expert outputs).  Survivors detect it within that call
+    (failure timeout on its combine flag), and tg_failover recomputes the pairs they had sent it
+    on the shadows: the repaired output of THAT call must be bitwise the unfailed output.  With
+    2 ranks every shadow of the dead rank's experts is on the survivor (spread placement)."""
+    import time
+    ok = True
+    dead = world - 1
+    tg.tg_set_failure_timeout(layer.ctx, 50.0)
+    dist.barrier()
+    if rank == dead:
+        tg.tg_inject_failure(layer.ctx)
+        layer(xr)
+        torch.cuda.synchronize()
+        rep["inflight_dead"] = dead
+    else:
+        t0 = time.perf_counter()
+        o = layer(xr)
+        rc, failed = layer.failover(xr, o)
+        torch.cuda.synchronize()
+        rep["failover_ms"] = round((time.perf_counter() - t0) * 1e3, 2)
+        if failed != (1 << dead):
+            ok = False
+            msgs.append(f"rank {rank}: failed mask {failed:#x}, expected {1 << dead:#x}")
+        if world == 2:
+            if rc != tg.TG_OK:
+                ok = False
+                msgs.append(f"rank {rank}: failover rc {rc}")
+            if not torch.equal(out.view(torch.int16), o.view(torch.int16)):
+                ok = False
+                msgs.append(f"rank {rank}: repaired output differs ({int((out != o).sum())} elements)")
+        # the next calls run without the dead rank (fail-stop, NEXT-3a)
+        for i in range(3):
+            o2 = run()
+            if not torch.equal(out.view(torch.int16), o2.view(torch.int16)):
+                ok = False
+                msgs.append(f"rank {rank}: call {i} after the failover differs")
+        rc2, f2 = layer.failover(xr, o2)
+        if f2 != 0:
+            ok = False
+            msgs.append(f"rank {rank}: spurious failure {f2:#x} after masking")
+        rep["inflight_rc"] = int(rc)
     dist.barrier()
     return ok
 

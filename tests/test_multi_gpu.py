@@ -45,3 +45,12 @@ def test_rank_fail_stop(config):
     G = torch.cuda.device_count()
     rep = _run(G, "--config", config, "--rank-fail")
     assert rep["rank_fail_dead"] == G - 1
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("config", ["tiny", "mixtral_decode"])
+def test_inflight_failover(config):
+    """NEXT-1: a rank crashes mid-call; the survivors repair that very call (tg_failover)."""
+    G = torch.cuda.device_count()
+    rep = _run(G, "--config", config, "--inflight-fail")
+    assert "inflight_rc" in rep or G > 2
