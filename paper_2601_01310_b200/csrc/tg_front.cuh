@@ -545,7 +545,7 @@ __device__ __forceinline__ void copy_row(uint4 *__restrict__ dst, const uint4 *_
 // during this latency-bound kernel.  Issued after the router's own loads so the
 // HBM queues serve those first.
 __device__ void l2_prefetch_share(const CallArgs &a, int part, int nparts) {
-  // issued by warp 1: thread 0's __threadfence in the arrival must not wait for these
+  // issued by warp 1 (thread 0 runs the arrivals of the front chain)
   if (threadIdx.x != 32 || a.l2_prefetch_bytes <= 0) return;
   int s0 = -1;
   for (int s = 0; s < a.S_loc && s0 < 0; ++s)
@@ -598,10 +598,13 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
         if (it < 5) TG_STAMP(20 + 2 * it);
         router_item(a, R, grp, kp, it == 0);
         if (it < 5) TG_STAMP(21 + 2 * it);
-        if (it == 0) l2_prefetch_share(a, blockIdx.x, min(bpp, ngroups) * nkp);
         if (chain) group_arrive(a, rk, grp, nkp, ngroups, R.part);
       }
     }
+    // every CTA issues its share of the L2 prefetch, behind the router's own loads: the router
+    // CTAs after their item (and its top-k chain), the idle ones after a short delay
+    if (!(slot < bpp && slot < ngroups)) __nanosleep(2000);
+    l2_prefetch_share(a, blockIdx.x, gridDim.x);
     if (!chain) {
       const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
       grid_barrier_z(gbar, nbar++, a.err);
