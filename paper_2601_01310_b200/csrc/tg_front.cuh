@@ -15,9 +15,9 @@
 //                 receive layout on every destination.
 //   P4 dispatch : 16-B vector copies of token rows into the destination rank's
 //                 receive buffer (peer memory) + origin metadata, then a
-//                 per-source data-ready flag (§4.2).  Runs on the
-//                 non-TMA/MMA warps of k_layer while the TMA producer already
-//                 streams the first weight tiles.
+//                 per-source data-ready flag (§4.2).  All warps of
+//                 k_layer, right after P3; the TMA producer then streams the
+//                 first weight tiles while the peers' rows are still landing.
 #pragma once
 #include <algorithm>
 

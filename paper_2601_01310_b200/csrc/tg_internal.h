@@ -101,7 +101,8 @@ struct CallArgs {
   int replay;            // 1: recompute pairs routed to failed ranks (key_old) on this rank's shadows
   uint32_t failed;       // replay: ranks whose pairs are recomputed
   const int32_t *key_old;  // replay: the failed call's destination keys
-  int inject_fail;       // fault injection (tests): stop after the dispatch, as a crash mid-call
+  int inject_fail;
+  int dev_flag;          // development A/B switch (TG_DEVFLAG)       // fault injection (tests): stop after the dispatch, as a crash mid-call
   // inputs / outputs
   const bf16 *x;
   bf16 *out;
