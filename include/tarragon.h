@@ -173,6 +173,28 @@ tg_status tg_failover(tg_ctx *ctx, const void *x, void *out, int n_tokens, void 
  * only tg_finalize may follow.                                               */
 tg_status tg_inject_failure(tg_ctx *ctx);
 
+/* KV-cache checkpointing in the AW-EW idle gaps (§6.1; segment
+ * size C = 2 H_kv (d / H_attn) S_elem, App. C: 4 KB per token and
+ * layer for Mixtral).  The checkpoint store of this AW is a pinned host bucket
+ * written by the copy engines (no SM time, no NVLink: the layer's traffic is
+ * untouched).  tg_kv_store_init(ctx, bytes) allocates it.
+ * tg_kv_checkpoint(ctx, seg, bytes, offset, seq, stream) enqueues, ordered
+ * after the work already on `stream` (the layer call that produced the
+ * segment), a copy of `bytes` from DEVICE `seg` to bucket + offset on a
+ * lowest-priority stream, then a commit record: seq becomes the committed
+ * sequence number once that copy (and every earlier one) has landed ("async
+ * log + commit record").  Non-blocking; seq must increase.
+ * tg_kv_committed(ctx, &seq): last committed seq (0: none yet).
+ * tg_kv_restore(ctx, dst, bytes, offset, stream): waits for the pending
+ * checkpoints, then copies bucket + offset back to DEVICE `dst` on `stream`
+ * (request-level restoration).  Errors: TG_ERR_NOT_LOADED (no
+ * store), TG_ERR_INVALID (range), TG_ERR_STALE_VERSION (seq not increasing),
+ * TG_ERR_UNSUPPORTED (host-only ctx), TG_ERR_OOM.                          */
+tg_status tg_kv_store_init(tg_ctx *ctx, size_t bytes);
+tg_status tg_kv_checkpoint(tg_ctx *ctx, const void *seg, size_t bytes, size_t offset, uint64_t seq, void *stream);
+tg_status tg_kv_committed(tg_ctx *ctx, uint64_t *seq);
+tg_status tg_kv_restore(tg_ctx *ctx, void *dst, size_t bytes, size_t offset, void *stream);
+
 /* One MoE layer round trip (collective: every live rank calls it, same order).
  * x: device bf16 [n_tokens][d] (this rank's tokens); out: device bf16
  * [n_tokens][d], must not alias x.  n_tokens <= max_tokens_per_rank (may be

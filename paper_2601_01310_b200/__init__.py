@@ -57,6 +57,10 @@ _SIG = {
     "tg_set_failure_timeout": ([_P, ctypes.c_double], _I),
     "tg_failover": ([_P, _P, _P, _I, _P, ctypes.POINTER(ctypes.c_uint32)], _I),
     "tg_inject_failure": ([_P], _I),
+    "tg_kv_store_init": ([_P, ctypes.c_size_t], _I),
+    "tg_kv_checkpoint": ([_P, _P, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint64, _P], _I),
+    "tg_kv_committed": ([_P, ctypes.POINTER(ctypes.c_uint64)], _I),
+    "tg_kv_restore": ([_P, _P, ctypes.c_size_t, ctypes.c_size_t, _P], _I),
     "tg_moe_layer": ([_P, _P, _P, _I, _P], _I),
     "tg_moe_layer_host": ([_P, _P, _P, _I, _P], _I),
     "tg_get_routing": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
@@ -193,6 +197,28 @@ def tg_failover(ctx, x: torch.Tensor, out: torch.Tensor, stream=None):
                           ctypes.byref(f))
     _check(ctx, rc, "tg_failover", ok=(TG_OK, TG_ERR_NO_ROUTE))
     return rc, int(f.value)
+
+
+def tg_kv_store_init(ctx, nbytes: int) -> int:
+    return _check(ctx, _lib.tg_kv_store_init(ctx, int(nbytes)), "tg_kv_store_init")
+
+
+def tg_kv_checkpoint(ctx, seg: torch.Tensor, offset: int, seq: int, stream=None) -> int:
+    """Checkpoint the device tensor `seg` (contiguous) at bucket offset `offset` with sequence number seq."""
+    nbytes = seg.numel() * seg.element_size()
+    return _check(ctx, _lib.tg_kv_checkpoint(ctx, _ptr(seg), nbytes, int(offset), int(seq), _stream(stream)),
+                  "tg_kv_checkpoint")
+
+
+def tg_kv_committed(ctx) -> int:
+    v = ctypes.c_uint64(0)
+    _check(ctx, _lib.tg_kv_committed(ctx, ctypes.byref(v)), "tg_kv_committed")
+    return int(v.value)
+
+
+def tg_kv_restore(ctx, dst: torch.Tensor, offset: int, stream=None) -> int:
+    nbytes = dst.numel() * dst.element_size()
+    return _check(ctx, _lib.tg_kv_restore(ctx, _ptr(dst), nbytes, int(offset), _stream(stream)), "tg_kv_restore")
 
 
 def tg_moe_layer(ctx, x: torch.Tensor, out: torch.Tensor, stream=None) -> int:

@@ -88,6 +88,15 @@ struct tg_ctx {
   int32_t *key_main = nullptr, *key_replay = nullptr;
   long long fail_timeout_ns = 200000000LL;  // in-call failure detection on data / combine flags
   bool inject_next = false;                 // fault injection for tests (tg_inject_failure)
+  // KV checkpoint store (NEXT-4): pinned host bucket written by the copy engines
+  uint8_t *kv_bucket = nullptr;
+  size_t kv_bytes = 0;
+  cudaStream_t kv_stream = nullptr;
+  cudaEvent_t kv_ev = nullptr;
+  volatile uint64_t kv_committed = 0;
+  static constexpr int kKvRecs = 4096;
+  struct KvRec { tg_ctx *c; uint64_t seq; } kv_rec[kKvRecs];
+  int kv_next = 0;
   int last_T = 0;
   int last_launches = 0;
   bool sticky = false;
@@ -760,6 +769,69 @@ int tg_last_launch_count(const tg_ctx *c) { return c ? c->last_launches : 0; }
 
 const char *tg_last_error(const tg_ctx *c) { return c ? c->errmsg.c_str() : g_init_error.c_str(); }
 
+// ------------------------------------------------------------ KV checkpointing (NEXT-4)
+tg_status tg_kv_store_init(tg_ctx *c, size_t bytes) {
+  if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device)");
+  if (c->kv_bucket) return fail(c, TG_ERR_INVALID, "checkpoint store already initialised");
+  if (bytes == 0) return fail(c, TG_ERR_INVALID, "empty checkpoint store");
+  CK(cudaSetDevice(c->device));
+  if (cudaHostAlloc(&c->kv_bucket, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    c->kv_bucket = nullptr;
+    return fail(c, TG_ERR_OOM, "pinned checkpoint bucket of %zu bytes", bytes);
+  }
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // lo = least urgent
+  CK(cudaStreamCreateWithPriority(&c->kv_stream, cudaStreamNonBlocking, lo));
+  CK(cudaEventCreateWithFlags(&c->kv_ev, cudaEventDisableTiming));
+  c->kv_bytes = bytes;
+  c->kv_committed = 0;
+  return TG_OK;
+}
+
+static void CUDART_CB kv_commit_cb(void *p) {
+  tg_ctx::KvRec *r = static_cast<tg_ctx::KvRec *>(p);
+  r->c->kv_committed = r->seq;  // stream order: every earlier segment has landed
+}
+
+tg_status tg_kv_checkpoint(tg_ctx *c, const void *seg, size_t bytes, size_t offset, uint64_t seq, void *stream) {
+  if (!c) return TG_ERR_INVALID;
+  if (!c->kv_bucket) return fail(c, TG_ERR_NOT_LOADED, "no checkpoint store (tg_kv_store_init)");
+  if (!seg || offset > c->kv_bytes || bytes > c->kv_bytes - offset)
+    return fail(c, TG_ERR_INVALID, "segment [%zu, +%zu) outside the %zu-byte bucket", offset, bytes, c->kv_bytes);
+  if (seq <= c->kv_rec[(c->kv_next + tg_ctx::kKvRecs - 1) % tg_ctx::kKvRecs].seq && c->kv_next > 0)
+    return fail(c, TG_ERR_STALE_VERSION, "sequence numbers must increase");
+  CK(cudaSetDevice(c->device));
+  // ordered after the work on `stream` (the layer call that produced the segment), then the
+  // copy engine and the commit record on the low-priority checkpoint stream
+  CK(cudaEventRecord(c->kv_ev, reinterpret_cast<cudaStream_t>(stream)));
+  CK(cudaStreamWaitEvent(c->kv_stream, c->kv_ev, 0));
+  CK(cudaMemcpyAsync(c->kv_bucket + offset, seg, bytes, cudaMemcpyDeviceToHost, c->kv_stream));
+  tg_ctx::KvRec *r = &c->kv_rec[c->kv_next % tg_ctx::kKvRecs];
+  ++c->kv_next;
+  r->c = c;
+  r->seq = seq;
+  CK(cudaLaunchHostFunc(c->kv_stream, kv_commit_cb, r));
+  return TG_OK;
+}
+
+tg_status tg_kv_committed(tg_ctx *c, uint64_t *seq) {
+  if (!c || !seq) return TG_ERR_INVALID;
+  *seq = c->kv_committed;
+  return TG_OK;
+}
+
+tg_status tg_kv_restore(tg_ctx *c, void *dst, size_t bytes, size_t offset, void *stream) {
+  if (!c) return TG_ERR_INVALID;
+  if (!c->kv_bucket) return fail(c, TG_ERR_NOT_LOADED, "no checkpoint store (tg_kv_store_init)");
+  if (!dst || offset > c->kv_bytes || bytes > c->kv_bytes - offset)
+    return fail(c, TG_ERR_INVALID, "segment [%zu, +%zu) outside the %zu-byte bucket", offset, bytes, c->kv_bytes);
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->kv_stream));  // restore only committed state
+  CK(cudaMemcpyAsync(dst, c->kv_bucket + offset, bytes, cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream)));
+  return TG_OK;
+}
+
 tg_status tg_finalize(tg_ctx *c) {
   if (!c) return TG_OK;
   if (!c->host_only) {
@@ -772,6 +844,9 @@ tg_status tg_finalize(tg_ctx *c) {
     cudaFree(c->sym); cudaFree(c->scratch); cudaFree(c->trace);
     if (c->err_host) cudaFreeHost(c->err_host);
     for (auto &e : c->ev) cudaEventDestroy(e);
+    if (c->kv_stream) cudaStreamDestroy(c->kv_stream);
+    if (c->kv_ev) cudaEventDestroy(c->kv_ev);
+    if (c->kv_bucket) cudaFreeHost(c->kv_bucket);
   }
   delete c;
   return TG_OK;

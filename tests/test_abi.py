@@ -133,3 +133,13 @@ def test_bank_slots_consecutive_per_rank():
     assert [tg.tg_bank_slot(ctx, ew, 0) for ew in range(4)] == [0, pl.slots_per_ew, 0, pl.slots_per_ew]
     assert tg.tg_bank_slot(ctx, 0, pl.slots_per_ew) == -1
     tg.tg_finalize(ctx)
+
+
+def test_kv_store_host_only_refused():
+    """NEXT-4: the checkpoint store needs a device (copy engines); host-only ctx refuses it."""
+    tg, ctx, pl = _host_ctx()
+    with pytest.raises(tg.TarragonError) as ei:
+        tg.tg_kv_store_init(ctx, 1 << 20)
+    assert ei.value.status == tg.TG_ERR_UNSUPPORTED
+    assert tg.tg_kv_committed(ctx) == 0
+    tg.tg_finalize(ctx)
