@@ -143,6 +143,24 @@ def test_tile_modes_parity(cfg, T, mode, monkeypatch):
         _big(cfg, 2004, n_sample=16, W=4 if cfg == "qwen_prefill" else 2)
 
 
+@pytest.mark.parametrize("cfg", ["tiny", "mixtral_decode"])
+def test_dual_and_single_gemm2_bitwise_equal(cfg, monkeypatch):
+    """Two W2 tiles per GEMM2 unit (default) or one (TG_G2DUAL=0): every output element sees the
+    same MMAs in the same K order, so the outputs are bitwise equal."""
+    tg = _tg()
+    sh = wl.CONFIGS[cfg]
+    L = wl.make_layer(sh, 1010)
+    x = wl.make_tokens(sh, 1010)
+    pl = wl.make_placement(sh.E, 2, 1)
+    outs = []
+    for dual in ("0", "1"):
+        monkeypatch.setenv("TG_G2DUAL", dual)
+        layer = tg.MoELayer(sh, pl, L, max_tokens_per_rank=sh.T)
+        outs.append(_run(layer, x).view(torch.int16).clone())
+        layer.close()
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_empty_call_and_errors():
     tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1004, T=16, T_max=64)
     empty = torch.empty(0, sh.d, dtype=torch.bfloat16, device="cuda")
