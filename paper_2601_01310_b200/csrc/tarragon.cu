@@ -259,6 +259,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t off = 0;
   L.recv = off; off = align_up(off + (size_t)c->R_tot * d * 2, 1024);
   L.meta = off; off = align_up(off + (size_t)c->R_tot * 8, 1024);
+  L.dup = off; off = align_up(off + (size_t)c->R_tot * 4, 1024);
   L.ybuf = off; off = align_up(off + Tm * k * d * 2, 1024);
   L.cnt_all = off; off = align_up(off + (size_t)2 * world * c->nkeys * 4, 1024);
   L.flags = off; off = align_up(off + kNumFlagKinds * kMaxWorld * 4, 1024);

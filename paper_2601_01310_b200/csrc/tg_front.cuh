@@ -412,6 +412,7 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
       a.sent_to[tid] = any > 0;
     }
     for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[k0 + s];
+    if (tid == 0) a.sync[5] = 0;  // no token dedup without peers
     return;
   }
   // all-gather: my totals -> cnt_all[par][rank][*] on every live peer, then release flags
@@ -442,6 +443,15 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
     a.gcounts[K] = g;
   }
   __syncthreads();
+  // token dedup (NEXT-2) for calls that move many rows (prefill): every rank takes the same
+  // decision from the same all-gathered counts (global pairs x row bytes >= 16 MB)
+  if (tid < 32) {
+    long long tot_pairs = 0;
+    for (int K = tid; K < nkeys; K += 32) tot_pairs += gsum[K];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot_pairs += __shfl_xor_sync(0xffffffffu, tot_pairs, o);
+    if (tid == 0) a.sync[5] = (tot_pairs * a.d * 2 >= (16ll << 20)) ? 1 : 0;
+  }
   // dbase[K] = rows of lower slots on that rank (all sources) + rows of lower sources
   for (int K = tid; K < nkeys; K += blockDim.x) {
     const int q = K / a.S_max, s = K % a.S_max;
@@ -522,13 +532,14 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
 // --------------------------------------------------------------------- P4
 // Warp copy of one row of nch 16-B chunks: up to 16 loads of a lane in flight
 // before its stores (the copy is latency-bound per warp).
+template <bool kCoherent = false>
 __device__ __forceinline__ void copy_row(uint4 *__restrict__ dst, const uint4 *__restrict__ src, int nch, int lane) {
   for (int c0 = lane; c0 < nch; c0 += 16 * 32) {
     uint4 v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int c = c0 + 32 * u;
-      if (c < nch) v[u] = __ldg(src + c);
+      if (c < nch) v[u] = kCoherent ? __ldcg(src + c) : __ldg(src + c);  // rows written by peers: L2
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
@@ -576,7 +587,7 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   TG_STAMP(0);
   // ---- P1 router (+ reset of the GEMM counters of this call)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x < 4) a.sync[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
   TG_STAMP(8);
   const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
   {
@@ -639,7 +650,7 @@ __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys 
   if (blockIdx.x == 0 && threadIdx.x == 0)
     *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x < 4) a.sync[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
   int nbar = 0;
   const int npairs = a.T * a.k;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
@@ -670,6 +681,7 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) 
   const int k = a.k, nch = a.d >> 3;
   const int npairs = a.T * k;
   const int nsh = (a.Fsh > 0 && !a.replay) ? a.T : 0;  // a replay keeps the shared expert's output
+  const bool dedup = __ldcg(a.sync + 5) != 0;
   for (int p = w; p < npairs + nsh; p += nw) {
     if (p < npairs) {
       const int t = p / k;
@@ -678,12 +690,29 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) 
       const int q = K / a.S_max;
       const int pos =
           __ldcg(a.dbase + K) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K) + __ldcg(a.lrank + p);
-      const uint4 *src = reinterpret_cast<const uint4 *>(a.x + (size_t)t * a.d);
-      uint4 *dst = reinterpret_cast<uint4 *>(a.sym[q] + a.L.recv) + (size_t)pos * nch;
-      copy_row(dst, src, nch, lane);
+      // token dedup (NEXT-2): a token goes once to each PEER rank; a later pair of the same
+      // token to the same peer only names the row the peer copies locally (HBM, not NVLink)
+      int from = -1;
+      if (q != a.rank && dedup) {
+        const int j = p - t * k;
+        for (int j2 = 0; j2 < j; ++j2) {
+          const int K2 = __ldcg(a.key + (size_t)t * k + j2);
+          if (K2 >= 0 && K2 / a.S_max == q) {
+            from = __ldcg(a.dbase + K2) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K2) +
+                   __ldcg(a.lrank + (size_t)t * k + j2);
+            break;
+          }
+        }
+      }
+      if (from < 0) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.x + (size_t)t * a.d);
+        uint4 *dst = reinterpret_cast<uint4 *>(a.sym[q] + a.L.recv) + (size_t)pos * nch;
+        copy_row(dst, src, nch, lane);
+      }
       if (lane == 0) {
         int2 *meta = reinterpret_cast<int2 *>(a.sym[q] + a.L.meta);
         meta[pos] = make_int2(a.rank, p);
+        reinterpret_cast<int32_t *>(a.sym[q] + a.L.dup)[pos] = from;
         a.dst_pos[p] = pos;
       }
     } else {
@@ -692,6 +721,20 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) 
       uint4 *dst = reinterpret_cast<uint4 *>(a.sym[a.rank] + a.L.recv) + (size_t)(a.R_sh0 + t) * nch;
       copy_row(dst, src, nch, lane);
     }
+  }
+}
+
+// Token dedup, receiving side: once every source's rows have landed, rows that a
+// source sent once for several of its pairs are copied locally into the other
+// pairs' positions.  Warps w of nw (grid-wide numbering); the caller counts the
+// CTAs done on sync[4].
+__device__ __forceinline__ void dedup_copies(const CallArgs &a, int w, int nw, int nrecv) {
+  const int lane = threadIdx.x & 31, nch = a.d >> 3;
+  const int32_t *dup = reinterpret_cast<const int32_t *>(a.sym[a.rank] + a.L.dup);
+  uint4 *recv = reinterpret_cast<uint4 *>(a.sym[a.rank] + a.L.recv);
+  for (int r = w; r < nrecv; r += nw) {
+    const int from = __ldcg(dup + r);
+    if (from >= 0) copy_row<true>(recv + (size_t)r * nch, recv + (size_t)from * nch, nch, lane);
   }
 }
 

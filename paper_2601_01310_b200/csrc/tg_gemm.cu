@@ -43,6 +43,7 @@ struct GemmShared {
   uint32_t tmem_base;
   int red_last;
   int nstages, stage_bytes;  // ring geometry of this call (build_plan)
+  int nrecv;                 // routed rows received by this rank (dedup copies scan them)
   // slot plan of this call (routed slots, then the shared pseudo-slot)
   int NS, G1, total, ngroups;
   int nt[kMaxPlan];        // token tiles per slot
@@ -112,6 +113,7 @@ __device__ void build_plan(const CallArgs &a, GemmShared *P) {
     bred += (ns > 1) ? nt * ctiles : 0;
   }
   if (lane == 31) {
+    P->nrecv = br;  // after the scan loop: every routed slot's rows
     P->stage_bytes = 2 * kTileBytes + nbw * BK * 2;  // multiple of 2 KB: 1 KB swizzle-atom aligned
     P->nstages = min(kStages, kRingBytes / P->stage_bytes);
     P->g1off[NS] = bu1;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem = S->tmem_base;
   const int n_units = S->total;
   const int nstages = S->nstages, stage_bytes = S->stage_bytes;
+  const bool dedup = __ldcg(a.sync + 5) != 0;  // token dedup in this call (decided in P3)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -272,6 +275,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             } else if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) {
               atomicOr(a.fail_mask, 1u << src);  // its rows never landed: computed on stale data, discarded
             }
+          }
+        }
+        if (dedup) {  // and the rows the dedup copies fill in (all CTAs, sync[4])
+          const int *dd = a.sync + 4;
+          if (ld_acquire_gpu(dd) < (int)gridDim.x) {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_gpu(dd) < (int)gridDim.x)
+              if (globaltimer_ns() - t0 > kWaitTimeoutNs) device_fail(err, 0x4004);
           }
         }
         fence_proxy_async_global();
@@ -401,7 +412,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         umma_commit(&S->tfull[h]);
       }
     }
-  } else if (warp >= 4) {
+  } else {
+    // ===================== token dedup, receiving side (warps 2-7, multi-GPU) =====================
+    if (dedup) {
+      if (lane == 0) {
+        for (int src = 0; src < a.world; ++src) {
+          if (src == a.rank || !__ldcg(a.need_src + src)) continue;
+          const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
+                               a.fslot_data * kMaxWorld + src;
+          if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) atomicOr(a.fail_mask, 1u << src);
+        }
+      }
+      __syncwarp();
+      dedup_copies(a, blockIdx.x * 6 + (warp - 2), gridDim.x * 6, S->nrecv);
+      named_bar_sync(2, 192);
+      if (threadIdx.x == 64) {
+        __threadfence();
+        atomicAdd(a.sync + 4, 1);
+      }
+    }
+  }
+  if (warp >= 4) {
     // ===================== epilogue (128 threads) =====================
     const int q = warp & 3;            // TMEM lane quarter of this warp
     const int et = threadIdx.x - 128;  // 0..127

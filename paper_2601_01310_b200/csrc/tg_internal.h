@@ -72,6 +72,7 @@ struct TmaMaps {
 struct SymLayout {
   size_t recv;      // bf16 [R_cap][d]            dispatched token rows
   size_t meta;      // int2 [R_cap]               origin (src rank, t*k + j)
+  size_t dup;       // int32 [R_cap]              token dedup: recv row to copy this row from (-1: sent)
   size_t ybuf;      // bf16 [T_max][k][d]         expert outputs returned to this AW
   size_t cnt_all;   // int32 [2][world][nkeys]    all-gathered per-source counts
   size_t flags;     // uint32 [5][kMaxWorld]      cnt / data / comb epoch flags, replay data / comb
@@ -126,7 +127,7 @@ struct CallArgs {
   int32_t *sent_to;      // [kMaxWorld] this rank sends rows to dest
   int32_t *slot_rows;    // [S_loc] M_s on this rank
   int64_t *stats;        // [nkeys]
-  int32_t *sync;         // [0..3] counters (scheduler, CTAs done, dispatch blocks); u64 grid barriers at [8], [10]
+  int32_t *sync;         // [0..4] counters (scheduler, CTAs done, dispatch blocks, -, dedup copies), [5] dedup on; u64 grid barriers at [8], [10], [12]
   int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters
   int n_ctr_max;
   int32_t *n_units;      // [1] units of the last call (written by the GEMM, diagnostics)

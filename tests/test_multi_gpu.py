@@ -54,3 +54,13 @@ def test_inflight_failover(config):
     G = torch.cuda.device_count()
     rep = _run(G, "--config", config, "--inflight-fail")
     assert "inflight_rc" in rep or G > 2
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_prefill_multi_gpu_token_dedup():
+    """NEXT-2: a prefill-sized call (>= 16 MB of dispatched rows) sends each token once per peer
+    rank and the peer copies it into its other pairs' rows; parity, flips and masks unchanged,
+    and the G-GPU output bitwise equal to the 1-GPU run."""
+    G = torch.cuda.device_count()
+    rep = _run(G, "--config", "qwen_prefill", "--sample", "16")
+    assert rep["cross_G_bit_identical"]

@@ -65,8 +65,14 @@ def main():
         st = tr["front_stamps"]
         p4_us = (st[4] - st[3]) / 1e3
         rt = layer.routing(Tr)
-        remote_rows = int((rt["dst_rank"] != rank).sum().item())
-        remote_bytes = remote_rows * (sh.d * 2 + 8)
+        dr = rt["dst_rank"].long()
+        remote_pairs = int((dr != rank).sum().item())
+        # token dedup: one row per (token, remote rank); every pair still sends 8 B origin + 4 B dup
+        onehot = torch.zeros(dr.shape[0], world, dtype=torch.bool, device=dr.device)
+        onehot.scatter_(1, dr, True)
+        onehot[:, rank] = False
+        remote_rows = int(onehot.sum().item())
+        remote_bytes = remote_rows * sh.d * 2 + remote_pairs * 12
         v = torch.tensor([p4_us, remote_bytes, call_us], device=dev, dtype=torch.float64)
         allv = [torch.empty_like(v) for _ in range(world)]
         dist.all_gather(allv, v)
@@ -74,7 +80,7 @@ def main():
             p4 = max(float(t[0]) for t in allv)
             rb = [float(t[1]) for t in allv]
             rep = {"config": a.config, "n_gpus": world, "T_global": T, "dispatch_p4_us_max": p4,
-                   "remote_bytes_per_rank": rb,
+                   "remote_bytes_per_rank": rb, "dedup": True,
                    "dispatch_GBps_per_direction_per_gpu": (max(rb) / (p4 * 1e-6) / 1e9) if p4 > 0 else None,
                    "nvlink_frac_of_900": ((max(rb) / (p4 * 1e-6) / 1e9) / 900.0) if p4 > 0 else None,
                    "call_us_max": max(float(t[2]) for t in allv),
