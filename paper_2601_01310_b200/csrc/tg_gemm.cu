@@ -43,6 +43,7 @@ struct GemmShared {
   uint32_t tmem_base;
   int red_last;
   int nstages, stage_bytes;  // ring geometry of this call (build_plan)
+  bf16 *ydst[BN_MAX_EPI];    // GEMM2 epilogue: combine-buffer row of each token of the unit
   int nrecv;                 // routed rows received by this rank (dedup copies scan them)
   // slot plan of this call (routed slots, then the shared pseudo-slot)
   int NS, G1, total, ngroups;
@@ -490,6 +491,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       } else {
         const bool split = (U.nsplit > 1);
+        const bool direct = !split && !sh;  // y stored straight into the source AW's combine buffer
+        if (direct) {
+          // one origin lookup per token of the unit (not one per stored element: the loads would
+          // serialise behind the stores they may alias), then a table read from smem
+          for (int i = et; i < U.nrows; i += 128) {
+            const int2 o = meta[U.n0 + i];
+            S->ydst[i] = reinterpret_cast<bf16 *>(a.sym[o.x] + a.L.ybuf) + (size_t)o.y * a.d;
+          }
+          named_bar_sync(1, 128);
+        }
         for (int hh = 0; hh < (U.dual ? 2 : 1); ++hh) {  // dual: second W2 tile at +128 rows / columns
           const int mm = m + hh * BM;
           for (int c0 = 0; c0 < U.nrows; c0 += 32) {
@@ -507,9 +518,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   } else if (sh) {
                     a.ysh[(size_t)(row - a.R_sh0) * a.d + mm] = __float2bfloat16_rn(v);
                   } else {
-                    const int2 o = meta[row];
-                    bf16 *yb = reinterpret_cast<bf16 *>(a.sym[o.x] + a.L.ybuf);
-                    yb[(size_t)o.y * a.d + mm] = __float2bfloat16_rn(v);
+                    S->ydst[c0 + n][mm] = __float2bfloat16_rn(v);
                   }
                 }
               }
@@ -518,6 +527,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         tc_fence_before();
         mbar_arrive(&S->tempty[h]);
+        if (direct) named_bar_sync(1, 128);  // the table is rebuilt by the next unit
         if (split) {
           // fixed-order split-K reduction ((p0 + p1) + p2) + ... by the last split to finish
           __threadfence();

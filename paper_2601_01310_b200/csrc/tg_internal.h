@@ -28,7 +28,8 @@ constexpr int BK = 64;
 constexpr int BN_MAX = 256;
 constexpr int kStages = 8;                      // maximum ring depth (stage size set per call)
 constexpr int kTileBytes = 16384;               // 128 rows x 128 B
-constexpr int kRingBytes = 216 * 1024;          // stage ring: floor(216 KB / stage) stages
+constexpr int kRingBytes = 214 * 1024;          // stage ring: floor(214 KB / stage) stages
+constexpr int BN_MAX_EPI = 256;                 // token-tile width bound of the GEMM2 epilogue table
 constexpr int kSchedDepth = 8;
 constexpr int kGemmThreads = 256;               // w0 TMA, w1 MMA, w2 TMEM, w4-7 epilogue
 constexpr int kTmemCols = 512;                  // 2 accumulator buffers x 256 columns
