@@ -189,6 +189,15 @@ def layer_algorithmic_bytes(shape, slot_rows_active, R_local, T_local):
     return b
 
 
+def layer_algorithmic_flops(shape, R_local, T_local):
+    """k_layer FLOPs per launch on one rank: routed expert FFNs (3 matmuls of d x F per row),
+    the shared expert (3 of d x F_sh per token), the router (d x E_r per token)."""
+    f = 2 * R_local * 3 * shape.d * shape.F
+    f += 2 * T_local * 3 * shape.d * shape.F_sh
+    f += 2 * T_local * shape.d * (shape.E + shape.shared_gate)
+    return f
+
+
 def cpu_oracle_sample(shape, L_host, x_host, pl, n_tokens, n_threads):
     """Time the oracle (as it stands) on the first n_tokens of the batch: O1..O8."""
     import oracle
@@ -363,9 +372,21 @@ def main():
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(f"{cfg}:N{N}:T{T_glob}")
-    roof = {"bound": "hbm", "kernel": "k_layer (front + dispatch || grouped FFN + combine, one launch)", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-            "algorithmic_bytes_per_launch": gbytes, "kernel_ms": g_ms,
+    gflops = layer_algorithmic_flops(shape, R_local, T_r)
+    tflops = gflops / (g_ms / 1e3) / 1e12
+    # the bound is the roof the layer's arithmetic intensity hits first (ridge = peak FLOP/s /
+    # peak B/s); the step runs back to back, so the tensor roof is the sustained bf16 figure
+    tf_peak = tf_sus if tf_sus > 0 else tf
+    tensor_bound = gflops / gbytes > tf_peak * 1e12 / (hbm * 1e9)
+    roof = {"bound": "tensor" if tensor_bound else "hbm",
+            "kernel": "k_layer (front + dispatch || grouped FFN + combine, one launch)",
+            "achieved": tflops if tensor_bound else achieved, "peak": tf_peak if tensor_bound else hbm,
+            "unit": "TFLOP/s" if tensor_bound else "GB/s",
+            "frac": (tflops / tf_peak) if tensor_bound else (achieved / hbm),
+            "traffic": traffic, "peak_source": src + (" (bf16 sustained)" if tensor_bound else " (HBM copy)"),
+            "algorithmic_bytes_per_launch": gbytes, "algorithmic_flops_per_launch": gflops,
+            "hbm_GBps": achieved, "hbm_frac": achieved / hbm, "tensor_TFLOPs": tflops, "tensor_frac": tflops / tf_peak,
+            "kernel_ms": g_ms,
             "kernel_share_of_step": (g_ms / (ms_prof / args.steps)) if ms_prof else None,
             "profiled_ms_per_step": ms_prof / args.steps,
             "per_kernel_ms": kt}
