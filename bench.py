@@ -404,7 +404,7 @@ def main():
             n = int(min(xc.shape[0], max(n, n * 12.0 / max(dt, 1e-3))))
             v, dt = cpu_oracle_sample(shape, Lh, xc, pl, n, cores)
         cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-               "sample": f"first {n} tokens of one batch through O1-O8 (fp64, {cores} threads over tokens), "
+               "sample": f"first {n} tokens of the bench batches through O1-O8 (fp64, {cores} threads over tokens), "
                          f"{dt:.1f} s"}
 
     if rank == 0:
