@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--sample", type=int, default=0, help="oracle FFN on this many sampled tokens (0 = all)")
     ap.add_argument("--rank-fail", action="store_true",
                     help="fail-stop the last rank (tg_mask_rank) instead of the EW/flip checks")
+    ap.add_argument("--empty-rank", action="store_true",
+                    help="the last rank calls with 0 tokens: the others' outputs must not change")
     ap.add_argument("--inflight-fail", action="store_true",
                     help="the last rank crashes mid-call; survivors repair that call (tg_failover)")
     a = ap.parse_args()
@@ -100,6 +102,10 @@ def main():
         msgs.append(f"rank {rank}: run-to-run differs")
     if a.rank_fail:
         ok = rank_fail_checks(a, tg, layer, pl, sh, W, rank, world, dev, out, run, msgs, rep) and ok
+        finish(ok, rank, rep, msgs, layer, dev)
+        return
+    if a.empty_rank:
+        ok = empty_rank_checks(tg, layer, rank, world, out, xr, dev, msgs, rep) and ok
         finish(ok, rank, rep, msgs, layer, dev)
         return
     if a.inflight_fail:
@@ -188,6 +194,35 @@ def rank_fail_checks(a, tg, layer, pl, sh, W, rank, world, dev, out, run, msgs, 
     rep["rank_fail_dead"] = dead
     # the failed process is still alive for the harness: it meets the survivors only here
     dist.barrier()
+    return ok
+
+
+def empty_rank_checks(tg, layer, rank, world, out, xr, dev, msgs, rep):
+    """A rank with no tokens still takes part in the count exchange and serves its EWs; every
+    other rank's outputs are bitwise those of the full call (outputs do not depend on the layout)."""
+    ok = True
+    empty = world - 1
+    for i in range(3):
+        if rank == empty:
+            e = torch.empty(0, xr.shape[1], dtype=xr.dtype, device=dev)
+            rc = tg.tg_moe_layer(layer.ctx, e, torch.empty_like(e))
+            torch.cuda.synchronize()
+            if rc != tg.TG_OK:
+                ok = False
+                msgs.append(f"rank {rank}: empty call rc {rc}")
+        else:
+            o = layer(xr)
+            torch.cuda.synchronize()
+            if not torch.equal(out.view(torch.int16), o.view(torch.int16)):
+                ok = False
+                msgs.append(f"rank {rank}: output changed when rank {empty} had no tokens")
+    # and back to a full call
+    o = layer(xr)
+    torch.cuda.synchronize()
+    if not torch.equal(out.view(torch.int16), o.view(torch.int16)):
+        ok = False
+        msgs.append(f"rank {rank}: full call after empty calls differs")
+    rep["empty_rank"] = empty
     return ok
 
 

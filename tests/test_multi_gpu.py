@@ -64,3 +64,13 @@ def test_prefill_multi_gpu_token_dedup():
     G = torch.cuda.device_count()
     rep = _run(G, "--config", "qwen_prefill", "--sample", "16")
     assert rep["cross_G_bit_identical"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("config", ["tiny", "qwen_prefill"])
+def test_rank_with_no_tokens(config):
+    """A rank with T = 0 still exchanges counts and serves rows; the others' outputs are unchanged."""
+    G = torch.cuda.device_count()
+    args = ["--config", config, "--empty-rank"] + (["--sample", "16"] if config != "tiny" else [])
+    rep = _run(G, *args)
+    assert rep["empty_rank"] == G - 1
