@@ -342,12 +342,15 @@ def main():
     oh = [torch.empty_like(h).pin_memory() for h in xh]
     for i in range(args.warmup):
         tg.tg_moe_layer_host(layer.ctx, xh[i % NB], oh[i % NB], stream)
+    tg.tg_host_sync(layer.ctx, stream)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    tg.tg_host_sync(layer.ctx, stream)  # the timed copies start after e0
     for i in range(args.steps):
         rc = tg.tg_moe_layer_host(layer.ctx, xh[i % NB], oh[i % NB], stream)
         assert rc == tg.TG_OK, tg.tg_last_error(layer.ctx)
+    tg.tg_host_sync(layer.ctx, stream)  # ... and end before e1 (every output delivered)
     e1.record(stream)
     barrier()
     ms_e = torch.tensor([e0.elapsed_time(e1)], device=dev)

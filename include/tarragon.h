@@ -203,8 +203,14 @@ tg_status tg_kv_restore(tg_ctx *ctx, void *dst, size_t bytes, size_t offset, voi
  * the call.                                                                */
 tg_status tg_moe_layer(tg_ctx *ctx, const void *x, void *out, int n_tokens, void *stream);
 
-/* End-to-end form: x_host/out_host are pinned HOST buffers.  Enqueues the
- * H2D copy of x, the layer and the D2H copy of out on `stream`.            */
+/* End-to-end form: x_host/out_host are pinned HOST buffers.  The H2D copy of
+ * x and the D2H copy of out run on the ctx's own copy streams, pipelined over
+ * two staging buffers so that they overlap the layers of the neighbouring
+ * calls on `stream`.  The outputs (and the right to reuse x_host) are
+ * guaranteed once `stream` passes a later tg_host_sync(ctx, stream), which
+ * makes `stream` wait for every pending host-path copy and orders the next
+ * host-path copies after the work already on `stream`.                     */
+tg_status tg_host_sync(tg_ctx *ctx, void *stream);
 tg_status tg_moe_layer_host(tg_ctx *ctx, const void *x_host, void *out_host, int n_tokens,
                             void *stream);
 

@@ -63,6 +63,7 @@ _SIG = {
     "tg_kv_restore": ([_P, _P, ctypes.c_size_t, ctypes.c_size_t, _P], _I),
     "tg_moe_layer": ([_P, _P, _P, _I, _P], _I),
     "tg_moe_layer_host": ([_P, _P, _P, _I, _P], _I),
+    "tg_host_sync": ([_P, _P], _I),
     "tg_get_routing": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
     "tg_max_slots": ([_P], _I),
     "tg_bank_slot": ([_P, _I, _I], _I),
@@ -224,6 +225,11 @@ def tg_kv_restore(ctx, dst: torch.Tensor, offset: int, stream=None) -> int:
 def tg_moe_layer(ctx, x: torch.Tensor, out: torch.Tensor, stream=None) -> int:
     n = x.shape[0] if x is not None else 0
     return _lib.tg_moe_layer(ctx, _ptr(x), _ptr(out), n, _stream(stream))
+
+
+def tg_host_sync(ctx, stream=None) -> int:
+    """`stream` waits for every pending host-path copy (outputs of tg_moe_layer_host complete)."""
+    return _check(ctx, _lib.tg_host_sync(ctx, _stream(stream)), "tg_host_sync")
 
 
 def tg_moe_layer_host(ctx, x_host: torch.Tensor, out_host: torch.Tensor, stream=None) -> int:

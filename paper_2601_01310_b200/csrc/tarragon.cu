@@ -82,7 +82,10 @@ struct tg_ctx {
   bool tracing = false;
   int force_mode = -1;                           // TG_WIDE=0/1 (development A/B), -1 auto
   int force_dual = -1;                           // TG_G2DUAL=0/1 (development A/B), -1 auto
-  bf16 *x_stage = nullptr, *out_stage = nullptr;   // for tg_moe_layer_host
+  bf16 *x_stage[2] = {nullptr, nullptr}, *out_stage[2] = {nullptr, nullptr};  // tg_moe_layer_host, double-buffered
+  cudaStream_t hs_h2d = nullptr, hs_d2h = nullptr;  // host-path copy streams (overlap with the layer)
+  cudaEvent_t ev_h2d[2] = {}, ev_k[2] = {}, ev_d2h[2] = {}, ev_sync = nullptr, ev_sync2 = nullptr;
+  long long host_calls = 0;
   uint32_t epoch = 0;    // local kernel runs
   uint32_t xepoch = 0;   // calls (equal on every rank)
   int32_t *key_main = nullptr, *key_replay = nullptr;
@@ -291,7 +294,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t o_Hs = carve(Fsh > 0 ? Tm * Fsh * 2 : 0);
   size_t o_ws = carve(c->nsplit > 1 ? (size_t)c->nsplit * c->R_cap * d * 4 : 0);
   size_t o_ysh = carve(Fsh > 0 ? Tm * d * 2 : 0);
-  size_t o_xs = carve(Tm * d * 2), o_os = carve(Tm * d * 2);
+  size_t o_xs = carve(2 * Tm * d * 2), o_os = carve(2 * Tm * d * 2);
   CKI(cudaMalloc(&c->scratch, so));
   CKI(cudaMemset(c->scratch, 0, so));
   uint8_t *sb = reinterpret_cast<uint8_t *>(c->scratch);
@@ -317,7 +320,10 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   a.n_units = (int32_t *)(sb + o_nu);
   a.H = (bf16 *)(sb + o_H); a.Hs = Fsh > 0 ? (bf16 *)(sb + o_Hs) : nullptr;
   a.ws = c->nsplit > 1 ? (float *)(sb + o_ws) : nullptr; a.ysh = Fsh > 0 ? (bf16 *)(sb + o_ysh) : nullptr;
-  c->x_stage = (bf16 *)(sb + o_xs); c->out_stage = (bf16 *)(sb + o_os);
+  for (int i = 0; i < 2; ++i) {
+    c->x_stage[i] = (bf16 *)(sb + o_xs) + (size_t)i * Tm * d;
+    c->out_stage[i] = (bf16 *)(sb + o_os) + (size_t)i * Tm * d;
+  }
   a.L = L;
   {
     const char *e = getenv("TG_PDL");  // development switch for A/B timing; default on
@@ -658,17 +664,68 @@ tg_status tg_failover(tg_ctx *c, const void *x, void *out, int T, void *stream, 
   return TG_OK;
 }
 
+static tg_status host_path_init(tg_ctx *c) {
+  if (c->hs_h2d) return TG_OK;
+  CK(cudaStreamCreateWithFlags(&c->hs_h2d, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->hs_d2h, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_sync2, cudaEventDisableTiming));
+  return TG_OK;
+}
+
+// Host path, pipelined over two staging buffers: the H2D copy of call i+1 and the D2H copy
+// of call i run on their own streams while the layer of the neighbouring call runs on `stream`.
 tg_status tg_moe_layer_host(tg_ctx *c, const void *xh, void *oh, int T, void *stream) {
   if (!c) return TG_ERR_INVALID;
   if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device): no compute path");
   if (T < 0 || T > c->T_max) return fail(c, TG_ERR_INVALID, "n_tokens %d > max_tokens_per_rank %d", T, c->T_max);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(c->device));
-  const size_t b = (size_t)T * c->d * 2;
-  if (T > 0) CK(cudaMemcpyAsync(c->x_stage, xh, b, cudaMemcpyHostToDevice, s));
-  tg_status st = tg_moe_layer(c, c->x_stage, c->out_stage, T, stream);
+  tg_status st = host_path_init(c);
   if (st) return st;
-  if (T > 0) CK(cudaMemcpyAsync(oh, c->out_stage, b, cudaMemcpyDeviceToHost, s));
+  const int b = (int)(c->host_calls & 1);
+  const size_t bytes = (size_t)T * c->d * 2;
+  if (c->host_calls < 2) {  // first uses of the buffers: ordered after the work already on `stream`
+    CK(cudaEventRecord(c->ev_sync, s));
+    CK(cudaStreamWaitEvent(c->hs_h2d, c->ev_sync, 0));
+  } else {                  // x_stage[b] is free once the layer of call i-2 has run
+    CK(cudaStreamWaitEvent(c->hs_h2d, c->ev_k[b], 0));
+    CK(cudaStreamWaitEvent(s, c->ev_d2h[b], 0));  // out_stage[b] read out by call i-2's D2H
+  }
+  if (T > 0) CK(cudaMemcpyAsync(c->x_stage[b], xh, bytes, cudaMemcpyHostToDevice, c->hs_h2d));
+  CK(cudaEventRecord(c->ev_h2d[b], c->hs_h2d));
+  CK(cudaStreamWaitEvent(s, c->ev_h2d[b], 0));
+  st = tg_moe_layer(c, c->x_stage[b], c->out_stage[b], T, stream);
+  if (st) return st;
+  CK(cudaEventRecord(c->ev_k[b], s));
+  CK(cudaStreamWaitEvent(c->hs_d2h, c->ev_k[b], 0));
+  if (T > 0) CK(cudaMemcpyAsync(oh, c->out_stage[b], bytes, cudaMemcpyDeviceToHost, c->hs_d2h));
+  CK(cudaEventRecord(c->ev_d2h[b], c->hs_d2h));
+  ++c->host_calls;
+  return TG_OK;
+}
+
+tg_status tg_host_sync(tg_ctx *c, void *stream) {
+  if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device)");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  tg_status st = host_path_init(c);
+  if (st) return st;
+  // `stream` waits for every pending host-path copy ...
+  CK(cudaEventRecord(c->ev_sync2, c->hs_d2h));
+  CK(cudaStreamWaitEvent(s, c->ev_sync2, 0));
+  CK(cudaEventRecord(c->ev_sync2, c->hs_h2d));
+  CK(cudaStreamWaitEvent(s, c->ev_sync2, 0));
+  // ... and later host-path copies wait for what is on `stream` now
+  CK(cudaEventRecord(c->ev_sync, s));
+  CK(cudaStreamWaitEvent(c->hs_h2d, c->ev_sync, 0));
+  CK(cudaStreamWaitEvent(c->hs_d2h, c->ev_sync, 0));
   return TG_OK;
 }
 
@@ -846,6 +903,15 @@ tg_status tg_finalize(tg_ctx *c) {
     if (c->err_host) cudaFreeHost(c->err_host);
     for (auto &e : c->ev) cudaEventDestroy(e);
     if (c->kv_stream) cudaStreamDestroy(c->kv_stream);
+    if (c->hs_h2d) cudaStreamDestroy(c->hs_h2d);
+    if (c->hs_d2h) cudaStreamDestroy(c->hs_d2h);
+    for (int i = 0; i < 2; ++i) {
+      if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+      if (c->ev_k[i]) cudaEventDestroy(c->ev_k[i]);
+      if (c->ev_d2h[i]) cudaEventDestroy(c->ev_d2h[i]);
+    }
+    if (c->ev_sync) cudaEventDestroy(c->ev_sync);
+    if (c->ev_sync2) cudaEventDestroy(c->ev_sync2);
     if (c->kv_ev) cudaEventDestroy(c->kv_ev);
     if (c->kv_bucket) cudaFreeHost(c->kv_bucket);
   }

@@ -187,9 +187,20 @@ def test_host_entry_point_e2e():
     xh = x.pin_memory()
     oh = torch.empty_like(xh).pin_memory()
     assert tg.tg_moe_layer_host(layer.ctx, xh, oh) == tg.TG_OK
+    tg.tg_host_sync(layer.ctx)
     torch.cuda.synchronize()
     od = _run(layer, x)
     assert torch.equal(oh.view(torch.int16), od.cpu().view(torch.int16))
+    # pipelined calls over the two staging buffers, different inputs per call
+    xs = [wl.make_tokens(sh, 2000 + i).pin_memory() for i in range(5)]
+    ohs = [torch.empty_like(v).pin_memory() for v in xs]
+    for v, o in zip(xs, ohs):
+        assert tg.tg_moe_layer_host(layer.ctx, v, o) == tg.TG_OK
+    tg.tg_host_sync(layer.ctx)
+    torch.cuda.synchronize()
+    for v, o in zip(xs, ohs):
+        ref = _run(layer, v.cuda()).cpu()
+        assert torch.equal(o.view(torch.int16), ref.view(torch.int16))
 
 
 def _big(cfg, seed, n_sample, W=2, T=None):
