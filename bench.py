@@ -210,7 +210,7 @@ def cpu_oracle_sample(shape, L_host, x_host, pl, n_tokens, n_threads):
     t0 = time.perf_counter()
     wsg = wl.as_u16(L_host.wsg) if L_host.wsg is not None else None
     r = oracle.layer(xs, wl.as_u16(L_host.wg), shape.k, w1, w3, w2, pl.cand, pl.ew_rank, pl.slots_per_ew,
-                     np.zeros(pl.n_ews, np.uint8), 1, shared=sh, n_threads=n_threads,
+                     np.zeros(pl.n_ews, np.uint8), max(pl.ew_rank) + 1, shared=sh, n_threads=n_threads,
                      gate_mode=shape.gate_mode, wsg=wsg)
     dt = time.perf_counter() - t0
     assert r["rc"] == 0

@@ -6,7 +6,7 @@ for n in 2 4; do
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2990$n bench.py --gpus $n > gpurun_out/final/bench_N$n.log 2>&1
   grep '^{' gpurun_out/final/bench_N$n.log | tail -1 > gpurun_out/final/bench_mixtral_decode_N$n.json
 done
-for cfg in ds_v2_lite_decode qwen_prefill ds_v2_lite_decode_g1 qwen_prefill_sg; do
+for cfg in ds_v2_lite_decode qwen_prefill; do
   timeout 600 python bench.py --config $cfg --no-cpu-baseline > gpurun_out/final/b_$cfg.log 2>&1; tail -1 gpurun_out/final/b_$cfg.log > gpurun_out/final/bench_$cfg.json
 done
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29912 bench.py --gpus 2 --config qwen_prefill --no-cpu-baseline > gpurun_out/final/bq2.log 2>&1
@@ -20,3 +20,5 @@ grep '^{' gpurun_out/final/mp4f.log | tail -1 > gpurun_out/final/mp_inflight_fai
 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29916 tools/trace_mp.py > gpurun_out/final/trace_mp4.log 2>&1
 grep '^{' gpurun_out/final/trace_mp4.log > gpurun_out/final/trace_mp_mixtral_G4.jsonl
 for f in gpurun_out/final/*.json; do echo "$f: $(cut -c1-160 $f)"; done
+timeout 900 python bench.py --impl reference > gpurun_out/final/ref.log 2>&1; tail -1 gpurun_out/final/ref.log > gpurun_out/final/bench_reference_N1.json
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29917 bench.py --impl reference --gpus 2 > gpurun_out/final/ref2.log 2>&1; echo "ref N2 rc=$?"; grep '^{' gpurun_out/final/ref2.log | tail -1 | cut -c1-120
