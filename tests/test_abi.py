@@ -143,3 +143,18 @@ def test_kv_store_host_only_refused():
     assert ei.value.status == tg.TG_ERR_UNSUPPORTED
     assert tg.tg_kv_committed(ctx) == 0
     tg.tg_finalize(ctx)
+
+
+def test_failover_and_host_path_host_only():
+    """NEXT-1 host-side validation: failure-timeout range; a host-only ctx has no failover, host path
+    or fault injection target (no device)."""
+    tg, ctx, pl = _host_ctx(E=8, W=2, G=2, rank=0)
+    with pytest.raises(tg.TarragonError):
+        tg.tg_set_failure_timeout(ctx, 0.0)
+    with pytest.raises(tg.TarragonError):
+        tg.tg_set_failure_timeout(ctx, 5000.0)
+    assert tg.tg_set_failure_timeout(ctx, 50.0) == tg.TG_OK
+    assert tg._lib.tg_failover(ctx, None, None, 0, None, None) == tg.TG_ERR_UNSUPPORTED
+    assert tg._lib.tg_host_sync(ctx, None) == tg.TG_ERR_UNSUPPORTED
+    assert tg.tg_inject_failure(ctx) == tg.TG_OK  # a flag for the next call (none can run here)
+    tg.tg_finalize(ctx)
