@@ -14,9 +14,10 @@ grouped SwiGLU expert GEMMs -> combine) over one synthetic batch.
 Prints ONE JSON line (rank 0).  `value` = tokens/s over the K timed steps
 (CUDA events on the launching stream, barrier + synchronize on both sides, max
 over ranks).  `e2e` = the same metric through tg_moe_layer_host (pinned host
-x in, out back to host, copies inside the timed region).  `roofline` = the
-GEMM kernel's algorithmic HBM bytes per launch / its mean event-timed
-duration inside the timed region, against MEASURED_PEAKS.json.
+x in, out back to host, copies inside the timed region, pipelined over two
+staging buffers).  `roofline` = k_layer (one launch per call) against the roof
+its arithmetic intensity reaches first: algorithmic HBM bytes (or FLOPs) per
+launch / its mean event-timed duration, against MEASURED_PEAKS.json.
 `--impl reference` times the CPU oracle (the tier's reference arm) on a
 bounded sample of the same workload.
 """

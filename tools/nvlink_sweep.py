@@ -4,7 +4,7 @@
 
 For each global token count T, runs the layer, traces one call and reports per
 rank: bytes this rank stored into PEER receive buffers in the dispatch phase
-(P4 of the front kernel: rows whose destination rank != this rank, d*2 B each,
+(P4 of k_layer: rows whose destination rank != this rank, d*2 B each,
 + 8 B metadata), the P4 duration from device timestamps, and the resulting
 GB/s per direction; plus the whole-call latency.  Rank 0 prints one JSON line
 per T with the max over ranks of the P4 time (the exchange completes when the

@@ -1,4 +1,4 @@
-"""Timeline of the grouped GEMM kernel (GK4) from its device trace.
+"""Timeline of k_layer (front phases, grouped GEMM units, combine) from its device trace.
 
     python tools/trace_gemm.py [--config mixtral_decode] [--tokens 256]
 
@@ -42,7 +42,7 @@ def main():
     tr = tg.tg_get_trace(layer.ctx)
     st = tr["front_stamps"]
     if st[0] > 0:
-        print("front kernel (us from start): group0 top-k %.2f, chunk0 rank %.2f, exchange start %.2f end %.2f, "
+        print("front phases (us from start): group0 top-k %.2f, chunk0 rank %.2f, exchange start %.2f end %.2f, "
               "grid barrier %.2f, dispatch done %.2f" % tuple((st[i] - st[0]) / 1e3 if st[i] else -1
                                                              for i in (12, 13, 1, 14, 3, 4)))
         print("group 0: part arrivals", [round((v - st[0]) / 1e3, 2) if v else -1 for v in st[40:48]],
