@@ -307,7 +307,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   a.bank_w3 = c->bank_w3;
   {
     // L2 prefetch budget: ~60% of L2 for the weights the GEMM streams first (r01 A/B: 0 -> 522 us,
-    // 40% -> 512.9 us, 60% -> 511.3 us, 80% -> 511.6 us per Mixtral decode call)
+    // 40% -> 512.9 us, 60% -> 511.3 us, 75% -> 511.6 us per Mixtral decode call)
     const char *e = getenv("TG_L2PF");  // development override (bytes; 0 = off)
     a.l2_prefetch_bytes = e ? atoll(e) : (long long)(prop.l2CacheSize * 0.6);
   }
