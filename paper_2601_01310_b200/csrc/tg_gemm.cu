@@ -252,8 +252,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const bool dedup = __ldcg(a.sync + 5) != 0;  // token dedup in this call (decided in P3)
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===================== TMA producer =====================
+    {
+      // ===================== TMA producer (warp 0) =====================
+      // Lane 0 schedules (work items, stage barriers, expected bytes); the loads of a stage
+      // are issued by different lanes in parallel — lane 3i: weight tile, 3i+1: second weight
+      // tile, 3i+2: token tile of the stage's i-th K block — because one thread's TMA issues
+      // serialise (~0.4 us per box: tools/probes/tma_stream.cu, 40 GB/s per SM with one issuer,
+      // 70-127 with 2-6 lanes).
       const uint64_t pol_w1 = policy_evict_first();  // weight tiles streamed once (one token tile)
       const uint64_t pol_wn = policy_evict_last();   // weight tiles re-read by several token tiles
       const uint64_t pol_x = policy_evict_last();    // token tiles: re-read by every weight tile
@@ -262,49 +267,56 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // source's rows have landed (release/acquire on per-source
       // epoch flags, then ordered before async-proxy reads).
       bool data_ok = false;
-      int npend = 0;
-      int pst[kStages], pkb[kStages], pcnt[kStages], prow[kStages];
-      uint32_t pab[kStages], psub[kStages];
+      int npend = 0;  // pending token-tile loads, held by the lane that will issue them
+      int pst[kStages], pkb[kStages], prow[kStages];
+      uint32_t pab[kStages];
       const CUtensorMap *pmap[kStages];
       auto wait_data = [&]() {
-        for (int src = 0; src < a.world; ++src) {
-          if (__ldcg(a.need_src + src)) {
-            const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
-                                 a.fslot_data * kMaxWorld + src;
-            if (src == a.rank) {
-              wait_flag_ge_s(fl, a.fepoch, sys, err, 0x4001);
-            } else if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) {
-              atomicOr(a.fail_mask, 1u << src);  // its rows never landed: computed on stale data, discarded
+        if (lane == 0) {
+          for (int src = 0; src < a.world; ++src) {
+            if (__ldcg(a.need_src + src)) {
+              const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
+                                   a.fslot_data * kMaxWorld + src;
+              if (src == a.rank) {
+                wait_flag_ge_s(fl, a.fepoch, sys, err, 0x4001);
+              } else if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) {
+                atomicOr(a.fail_mask, 1u << src);  // its rows never landed: computed on stale data, discarded
+              }
+            }
+          }
+          if (dedup) {  // and the rows the dedup copies fill in (all CTAs, sync[4])
+            const int *dd = a.sync + 4;
+            if (ld_acquire_gpu(dd) < (int)gridDim.x) {
+              const uint64_t t0 = globaltimer_ns();
+              while (ld_acquire_gpu(dd) < (int)gridDim.x)
+                if (globaltimer_ns() - t0 > kWaitTimeoutNs) device_fail(err, 0x4004);
             }
           }
         }
-        if (dedup) {  // and the rows the dedup copies fill in (all CTAs, sync[4])
-          const int *dd = a.sync + 4;
-          if (ld_acquire_gpu(dd) < (int)gridDim.x) {
-            const uint64_t t0 = globaltimer_ns();
-            while (ld_acquire_gpu(dd) < (int)gridDim.x)
-              if (globaltimer_ns() - t0 > kWaitTimeoutNs) device_fail(err, 0x4004);
-          }
-        }
+        __syncwarp();
         fence_proxy_async_global();
         data_ok = true;
         for (int i = 0; i < npend; ++i)
-          for (int j = 0; j < pcnt[i]; ++j)
-            tma_load_2d(ring + pst[i] * stage_bytes + j * psub[i] + pab[i], pmap[i], &S->full[pst[i]],
-                        (pkb[i] + j) * BK, prow[i], pol_x);
+          tma_load_2d(ring + pst[i] * stage_bytes + pab[i], pmap[i], &S->full[pst[i]], pkb[i] * BK, prow[i], pol_x);
         npend = 0;
       };
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0;; ++it) {
-        int u = atomicAdd(&a.sync[1], 1);
-        if (u >= n_units) u = -1;
+        int u = 0;
+        if (lane == 0) {
+          u = atomicAdd(&a.sync[1], 1);
+          if (u >= n_units) u = -1;
+        }
+        u = __shfl_sync(0xffffffffu, u, 0);
         const int r = it % kSchedDepth;
-        mbar_wait(&S->sempty[r], ((it / kSchedDepth) & 1) ^ 1, err);
-        S->sched[r] = u;
-        mbar_arrive(&S->sfull[r]);
+        if (lane == 0) {
+          mbar_wait(&S->sempty[r], ((it / kSchedDepth) & 1) ^ 1, err);
+          S->sched[r] = u;
+          mbar_arrive(&S->sfull[r]);
+        }
         if (u < 0) {
-          if (!data_ok && npend > 0) wait_data();
+          if (!data_ok && __any_sync(0xffffffffu, npend > 0)) wait_data();
           break;
         }
         const Unit U = decode_unit(a, S, u);
@@ -313,7 +325,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (!g1) {
           if (!data_ok) wait_data();  // GEMM1 tiles waiting on pending B loads come first
           // all GEMM1 tiles of this (slot, n-tile) have written H
-          wait_ctr_ge(a.ctr + U.dep, U.dep_target, err, 0x4002);
+          if (lane == 0) wait_ctr_ge(a.ctr + U.dep, U.dep_target, err, 0x4002);
+          __syncwarp();
           fence_proxy_async_global();
         }
         const int bi = box_index(U.nrows);
@@ -328,23 +341,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int rowA = g1 ? U.slot * (sh ? a.Fsh : a.F) + U.m0 : U.slot * a.d + U.m0;
         const int rowB = (!g1 && sh) ? U.n0 - a.R_sh0 : U.n0;
         const uint64_t pol_w = (U.ntiles > 1) ? pol_wn : pol_w1;
+        const int li = lane / 3, role = lane % 3;  // K block of the stage / which load
         for (int kb = U.kb0; kb < U.kb1; kb += kps) {
           const int cnt = min(kps, U.kb1 - kb);
-          if (!data_ok && npend == nstages) wait_data();  // every stage holds a pending B tile
-          mbar_wait(&S->empty[stage], phase ^ 1, err);
-          uint8_t *st = ring + stage * stage_bytes;
-          mbar_arrive_expect_tx(&S->full[stage], (uint32_t)cnt * sub);
-          for (int i = 0; i < cnt; ++i) {
-            uint8_t *sb = st + i * sub;
-            tma_load_2d(sb, mA0, &S->full[stage], (kb + i) * BK, rowA, pol_w);
-            if (g1) tma_load_2d(sb + kTileBytes, mA1, &S->full[stage], (kb + i) * BK, rowA, pol_w);
-            else if (U.dual) tma_load_2d(sb + kTileBytes, mA0, &S->full[stage], (kb + i) * BK, rowA + BM, pol_w);
-            if (data_ok) tma_load_2d(sb + abytes, mB, &S->full[stage], (kb + i) * BK, rowB, pol_x);
+          if (!data_ok && __any_sync(0xffffffffu, npend == nstages)) wait_data();  // every stage holds a pending B tile
+          if (lane == 0) {
+            mbar_wait(&S->empty[stage], phase ^ 1, err);
+            mbar_arrive_expect_tx(&S->full[stage], (uint32_t)cnt * sub);
           }
-          if (!data_ok) {
-            pst[npend] = stage; pkb[npend] = kb; pcnt[npend] = cnt; prow[npend] = rowB;
-            pab[npend] = abytes; psub[npend] = sub; pmap[npend] = mB;
-            ++npend;
+          __syncwarp();
+          uint8_t *sb = ring + stage * stage_bytes + li * sub;
+          if (li < cnt) {
+            const int kk = (kb + li) * BK;
+            if (role == 0) {
+              tma_load_2d(sb, mA0, &S->full[stage], kk, rowA, pol_w);
+            } else if (role == 1) {
+              if (g1) tma_load_2d(sb + kTileBytes, mA1, &S->full[stage], kk, rowA, pol_w);
+              else if (U.dual) tma_load_2d(sb + kTileBytes, mA0, &S->full[stage], kk, rowA + BM, pol_w);
+            } else if (data_ok) {
+              tma_load_2d(sb + abytes, mB, &S->full[stage], kk, rowB, pol_x);
+            } else {
+              pst[npend] = stage; pkb[npend] = kb + li; prow[npend] = rowB;
+              pab[npend] = li * sub + abytes; pmap[npend] = mB;
+              ++npend;
+            }
           }
           if (++stage == nstages) { stage = 0; phase ^= 1; }
         }
