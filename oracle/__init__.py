@@ -58,6 +58,12 @@ def lib():
         L.orc_shared_gate.argtypes = [P, P, i32, i32, P]
         L.orc_moe_tokens2.argtypes = [i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, i32, P, P, i32, P]
         L.orc_moe_tokens2.restype = i32
+        L.orc_moe_tokens3.argtypes = [i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P, i32, P, P, i32, P, P]
+        L.orc_moe_tokens3.restype = i32
+        L.orc_router_f64.argtypes = [P, P, i32, i32, i32, P, P]
+        L.orc_stage_h.argtypes = [P, i32, i32, i32, P, P, P, P, P, P, P, i32]
+        L.orc_stage_y.argtypes = [P, i32, i32, i32, P, P, P, i32]
+        L.orc_stage_combine.argtypes = [i32, i32, i32, P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -96,6 +102,54 @@ def router(x: np.ndarray, wg: np.ndarray) -> np.ndarray:
     out = np.empty((T, E), np.float32)
     lib().orc_router(_p(x), _p(wg), T, d, E, _p(out))
     return out
+
+
+def router_f64(x: np.ndarray, wg: np.ndarray):
+    """O1 before the fp32 rounding: (l_exact fp64 [T, E], sum of |x Wg| fp64 [T, E])."""
+    x, wg = _u16(x), _u16(wg)
+    T, d = x.shape
+    E = wg.shape[0]
+    l = np.empty((T, E), np.float64)
+    s = np.empty((T, E), np.float64)
+    lib().orc_router_f64(_p(x), _p(wg), T, d, E, _p(l), _p(s))
+    return l, s
+
+
+def stage_h(rows_x, w1, w3, n_threads=1):
+    """O6a on rows sharing one expert: dict(h, a1, a3, s1, s3), fp64 [n, F]; h = silu(a1) * a3 unrounded."""
+    rows_x, w1, w3 = _u16(rows_x), _u16(w1), _u16(w3)
+    n, d = rows_x.shape
+    F = w1.shape[0]
+    out = {k: np.empty((n, F), np.float64) for k in ("h", "a1", "a3", "s1", "s3")}
+    lib().orc_stage_h(_p(rows_x), n, d, F, _p(w1), _p(w3), *(_p(out[k]) for k in ("h", "a1", "a3", "s1", "s3")),
+                      int(n_threads))
+    return out
+
+
+def stage_y(rows_h, w2, n_threads=1):
+    """O6b on stored bf16 h rows sharing one expert: (y_exact fp64 [n, d], sum |h W2| fp64 [n, d])."""
+    rows_h, w2 = _u16(rows_h), _u16(w2)
+    n, F = rows_h.shape
+    d = w2.shape[0]
+    y = np.empty((n, d), np.float64)
+    s = np.empty((n, d), np.float64)
+    lib().orc_stage_y(_p(rows_h), n, d, F, _p(w2), _p(y), _p(s), int(n_threads))
+    return y, s
+
+
+def stage_combine(w, y, ysh=None, sg=None):
+    """O8 before the bf16 rounding: w fp32 [n, k], y bf16 [n, k, d], ysh bf16 [n, d] | None,
+    sg fp32 [n] | None -> (out_exact fp64 [n, d], sum of |terms| fp64 [n, d])."""
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    y = _u16(y)
+    n, k, d = y.shape
+    ysh = _u16(ysh) if ysh is not None else None
+    sg = np.ascontiguousarray(sg, dtype=np.float32) if sg is not None else None
+    out = np.empty((n, d), np.float64)
+    s = np.empty((n, d), np.float64)
+    lib().orc_stage_combine(n, d, k, _p(w), _p(y), _p(ysh) if ysh is not None else None,
+                            _p(sg) if sg is not None else None, _p(out), _p(s))
+    return out, s
 
 
 def select(logits: np.ndarray, k: int, gate_mode: int = 0):
@@ -152,8 +206,9 @@ def shared_gate(x, wsg) -> np.ndarray:
     return out
 
 
-def moe_tokens(x, idx, w, w1, w3, w2, shared=None, tokens=None, want_y=False, n_threads=1, sgate=None):
-    """O6-O8 for the given tokens (all if None).
+def moe_tokens(x, idx, w, w1, w3, w2, shared=None, tokens=None, want_y=False, n_threads=1, sgate=None,
+               want_f64=False):
+    """O6-O8 for the given tokens (all if None).  want_f64: also out before its bf16 rounding.
 
     w1/w3/w2: sequences of E bf16 arrays (W1, W3: [F, d]; W2: [d, F]).
     shared: optional (W1s, W3s, W2s) of the merged shared expert.
@@ -190,16 +245,19 @@ def moe_tokens(x, idx, w, w1, w3, w2, shared=None, tokens=None, want_y=False, n_
     y = np.empty((n, k, d), np.uint16) if want_y else None
     ysh = np.empty((n, d), np.uint16) if (want_y and shared is not None) else None
     sg = None if sgate is None else np.ascontiguousarray(sgate, dtype=np.float32)
-    rc = lib().orc_moe_tokens2(d, E, k, F, F_sh, _p(x), _p(idx), _p(w),
+    of = np.empty((n, d), np.float64) if want_f64 else None
+    rc = lib().orc_moe_tokens3(d, E, k, F, F_sh, _p(x), _p(idx), _p(w),
                                ctypes.cast(p1, ctypes.c_void_p), ctypes.cast(p3, ctypes.c_void_p),
                                ctypes.cast(p2, ctypes.c_void_p), ps[0], ps[1], ps[2],
                                _p(sg) if sg is not None else None,
                                _p(tok) if tok is not None else None, n, _p(out),
                                _p(y) if y is not None else None, int(n_threads),
-                               _p(ysh) if ysh is not None else None)
+                               _p(ysh) if ysh is not None else None,
+                               _p(of) if of is not None else None)
     if rc != OK:
         raise ValueError(f"orc_moe_tokens rc={rc}")
-    return (out, (y, ysh)) if want_y else out
+    res = (out, (y, ysh)) if want_y else out
+    return (res, of) if want_f64 else res
 
 
 def slot_bases(n_ews: int, ew_rank, slots_per_ew: int):
@@ -219,7 +277,8 @@ def layer(x, wg, k, w1, w3, w2, cand, ew_rank, slots_per_ew, mask, G, shared=Non
     """The whole path O1..O8 for global tokens ``x`` (contiguous split over G ranks).
 
     Returns a dict with logits, idx, w, gap, rank_e, bank_e, dst_rank,
-    dst_slot, dst_pos, counts, out (for ``tokens`` or all tokens), rc.
+    dst_slot, dst_pos, counts, out and out_f64 (out before its bf16 rounding; for
+    ``tokens`` or all tokens), y/ysh (want_y), rc.
     """
     logits = router(x, wg)
     idx, w, gap = select(logits, k, gate_mode)
@@ -236,8 +295,8 @@ def layer(x, wg, k, w1, w3, w2, cand, ew_rank, slots_per_ew, mask, G, shared=Non
     res.update(dst_rank=dr, dst_slot=ds, dst_pos=dp, counts=counts)
     sgate = shared_gate(x, wsg) if (wsg is not None and shared is not None) else None
     res["sgate"] = sgate
-    r = moe_tokens(x, idx, w, w1, w3, w2, shared=shared, tokens=tokens, n_threads=n_threads, want_y=want_y,
-                   sgate=sgate)
+    r, res["out_f64"] = moe_tokens(x, idx, w, w1, w3, w2, shared=shared, tokens=tokens, n_threads=n_threads,
+                                   want_y=want_y, sgate=sgate, want_f64=True)
     if want_y:
         res["out"], (res["y"], res["ysh"]) = r
     else:

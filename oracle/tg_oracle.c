@@ -117,12 +117,32 @@ void orc_router(const uint16_t *x, const uint16_t *wg, int T, int d, int E, floa
         }
 }
 
+/* O1 before its fp32 rounding (parity tests): l_exact[t][e] in fp64 and
+ * s[t][e] = sum_i |x Wg| (the scale of a floating-point evaluation's error). */
+void orc_router_f64(const uint16_t *x, const uint16_t *wg, int T, int d, int E, double *l, double *s) {
+    for (int t = 0; t < T; ++t)
+        for (int e = 0; e < E; ++e) {
+            double acc = 0.0, sa = 0.0;
+            for (int i = 0; i < d; ++i) {
+                double p = orc_bf16_to_f64(x[(int64_t)t * d + i]) * orc_bf16_to_f64(wg[(int64_t)e * d + i]);
+                acc += p;
+                sa += fabs(p);
+            }
+            l[(int64_t)t * E + e] = acc;
+            s[(int64_t)t * E + e] = sa;
+        }
+}
+
+
 /* ---------------------------------------------------- O2/O3 top-k, softmax */
 
 /* O2  S_t = the k experts first in the order (−l, e) ascending, i.e. largest
  *     logit first, equal logits broken by lowest expert id (R#3).  Slots j
  *     are the selected ids in ascending id order (R#4).
- *     gap_t = l_(k) − l_(k+1) in that order (0 if k == E).
+ *     gap_t = l_(k) − l_(k+1) in that order; +inf if k == E (there is no
+ *     (k+1)-th logit, so no selection can flip: the near-tie rule of the
+ *     north_star, "the k-th and (k+1)-th gate logits differ by less than
+ *     1e-5", never applies).
  * O3  w_j = exp(l_j − m) / sum_j' exp(l_j' − m), m = max selected logit,
  *     computed in fp64 from the fp32 logits and rounded once to fp32
  *     (R#1/R#2: softmax over the k selected logits = renormalised top-k).
@@ -156,7 +176,7 @@ int orc_select_mode(const float *logits, int T, int E, int k, int mode, int32_t 
             }
             int tmp = order[p]; order[p] = order[best]; order[best] = tmp;
         }
-        if (gap) gap[t] = (k < E) ? (l[order[k - 1]] - l[order[k]]) : 0.0f;
+        if (gap) gap[t] = (k < E) ? (l[order[k - 1]] - l[order[k]]) : INFINITY;
         /* ascending expert id within the selected set */
         for (int j = 0; j < k; ++j) sel[j] = order[j];
         for (int a = 1; a < k; ++a) {
@@ -257,41 +277,125 @@ int orc_permute(int T, int k, const int32_t *idx, const int32_t *rank_e, const i
  *       a1[f] = sum_i x[i] W1[f][i],  a3[f] = sum_i x[i] W3[f][i]   (fp64)
  *       h[f]  = bf16( silu(a1[f]) * a3[f] ),  silu(a) = a / (1 + exp(−a))
  *       y[c]  = bf16( sum_f h[f] W2[c][f] )                          (fp64)
- *     W1, W3: [F][d] row-major; W2: [d][F] row-major. */
-static void orc_ffn(const uint16_t *x, int d, int F, const uint16_t *W1, const uint16_t *W3,
-                    const uint16_t *W2, double *hbuf, uint16_t *y) {
+ *     W1, W3: [F][d] row-major; W2: [d][F] row-major.
+ * The two halves are exported separately (O6a, O6b) with their values BEFORE
+ * the bf16 storage rounding, so that the parity tests can check each storage
+ * point of the GPU path against the exact value computed from the GPU's own
+ * inputs to that stage (R#21).  s* = sums of |terms|: the scale of
+ * the accumulation error of a floating-point evaluation of the same sum. */
+
+/* O6a  one token row x [d]: h_exact[f] = silu(a1[f]) * a3[f] in fp64 (not
+ *      rounded); a1, a3, s1 = sum_i |x W1|, s3 = sum_i |x W3| (may be NULL). */
+void orc_ffn_h_f64(const uint16_t *x, int d, int F, const uint16_t *W1, const uint16_t *W3,
+                   double *h, double *a1o, double *a3o, double *s1o, double *s3o) {
     for (int f = 0; f < F; ++f) {
-        double a1 = 0.0, a3 = 0.0;
+        double a1 = 0.0, a3 = 0.0, s1 = 0.0, s3 = 0.0;
         const uint16_t *r1 = W1 + (int64_t)f * d, *r3 = W3 + (int64_t)f * d;
         for (int i = 0; i < d; ++i) {
             double xi = orc_bf16_to_f64(x[i]);
-            a1 += xi * orc_bf16_to_f64(r1[i]);
-            a3 += xi * orc_bf16_to_f64(r3[i]);
+            double p1 = xi * orc_bf16_to_f64(r1[i]), p3 = xi * orc_bf16_to_f64(r3[i]);
+            a1 += p1;
+            a3 += p3;
+            s1 += fabs(p1);
+            s3 += fabs(p3);
         }
         double silu = a1 / (1.0 + exp(-a1));
-        hbuf[f] = orc_bf16_to_f64(orc_bf16_from_f64(silu * a3));
+        h[f] = silu * a3;
+        if (a1o) a1o[f] = a1;
+        if (a3o) a3o[f] = a3;
+        if (s1o) s1o[f] = s1;
+        if (s3o) s3o[f] = s3;
     }
+}
+
+/* O6b  from the stored (bf16) h [F]: y_exact[c] = sum_f h[f] W2[c][f] in fp64
+ *      (not rounded); s[c] = sum_f |h[f] W2[c][f]| (may be NULL). */
+void orc_ffn_y_f64(const uint16_t *h, int d, int F, const uint16_t *W2, double *y, double *s) {
     for (int c = 0; c < d; ++c) {
-        double acc = 0.0;
+        double acc = 0.0, sa = 0.0;
         const uint16_t *r2 = W2 + (int64_t)c * F;
-        for (int f = 0; f < F; ++f) acc += hbuf[f] * orc_bf16_to_f64(r2[f]);
-        y[c] = orc_bf16_from_f64(acc);
+        for (int f = 0; f < F; ++f) {
+            double p = orc_bf16_to_f64(h[f]) * orc_bf16_to_f64(r2[f]);
+            acc += p;
+            sa += fabs(p);
+        }
+        y[c] = acc;
+        if (s) s[c] = sa;
     }
+}
+
+/* O6 = O6a, bf16 storage of h, O6b, bf16 storage of y.  y_exact (optional):
+ * y before its rounding.  hwork: [F] doubles, hbf: [F] bf16 scratch. */
+static void orc_ffn(const uint16_t *x, int d, int F, const uint16_t *W1, const uint16_t *W3,
+                    const uint16_t *W2, double *hwork, uint16_t *hbf, double *ywork, uint16_t *y) {
+    orc_ffn_h_f64(x, d, F, W1, W3, hwork, NULL, NULL, NULL, NULL);
+    for (int f = 0; f < F; ++f) hbf[f] = orc_bf16_from_f64(hwork[f]);
+    orc_ffn_y_f64(hbf, d, F, W2, ywork, NULL);
+    for (int c = 0; c < d; ++c) y[c] = orc_bf16_from_f64(ywork[c]);
+}
+
+/* Batched O6a / O6b over n rows that share one expert's weights (parity
+ * tests; OpenMP over rows only, the arithmetic per row is unchanged).
+ *   rows_x [n][d] bf16 -> h [n][F] fp64 (+ a1, a3, s1, s3 [n][F], optional)
+ *   rows_h [n][F] bf16 -> y [n][d] fp64 (+ s [n][d], optional)           */
+void orc_stage_h(const uint16_t *rows_x, int n, int d, int F, const uint16_t *W1, const uint16_t *W3,
+                 double *h, double *a1, double *a3, double *s1, double *s3, int n_threads) {
+#ifdef _OPENMP
+    if (n_threads < 1) n_threads = 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(n_threads)
+#endif
+    for (int r = 0; r < n; ++r) {
+        const int64_t o = (int64_t)r * F;
+        orc_ffn_h_f64(rows_x + (int64_t)r * d, d, F, W1, W3, h + o, a1 ? a1 + o : NULL, a3 ? a3 + o : NULL,
+                      s1 ? s1 + o : NULL, s3 ? s3 + o : NULL);
+    }
+}
+
+void orc_stage_y(const uint16_t *rows_h, int n, int d, int F, const uint16_t *W2, double *y, double *s,
+                 int n_threads) {
+#ifdef _OPENMP
+    if (n_threads < 1) n_threads = 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(n_threads)
+#endif
+    for (int r = 0; r < n; ++r)
+        orc_ffn_y_f64(rows_h + (int64_t)r * F, d, F, W2, y + (int64_t)r * d, s ? s + (int64_t)r * d : NULL);
 }
 
 /* -------------------------------------------------------- O8 combine */
 
-/* O6-O8 for a list of tokens.
- *   For token t (global index tokens[n]) and its k selected experts idx[t][j]
- *   with weights w[t][j]:  y_j = FFN_{e_j}(x_t)  (O6);  y_sh = FFN_sh(x_t) if
- *   F_sh > 0 (O7, R#16: shared expert added with weight 1);
- *   out[n][c] = bf16( sum_j w_j * y_j[c]  (+ y_sh[c]) )   in fp64, j order
- *   (O8, P:267 "aggregated via a weighted sum using the gating weights").
- *   The FFN of a pair depends only on (x_t, expert weights): which EW or
- *   slot serves it never enters (P:918 §5.1, stateless replay).
- * w1/w3/w2: arrays of E pointers to the per-expert matrices.
- * y_out (optional): [n_tokens][k][d] bf16 per-pair expert outputs.
- * n_threads > 1 parallelises over tokens only (arithmetic per token unchanged). */
+/* O8  one token: out_exact[c] = sum_j w_j * y_j[c] (+ sg * y_sh[c]) in fp64, j in
+ *     order, before the bf16 storage rounding of out ("aggregated via a
+ *     weighted sum using the gating weights"; R#5 on the AW; R#16 shared expert
+ *     with weight 1, or sg = sigmoid gate, O7').  y [k][d] and y_sh [d] bf16
+ *     (y_sh may be NULL); s[c] = sum of |terms| (may be NULL). */
+void orc_combine_f64(int d, int k, const float *w, const uint16_t *y, const uint16_t *ysh, double sg,
+                     double *out, double *s) {
+    for (int c = 0; c < d; ++c) {
+        double acc = 0.0, sa = 0.0;
+        for (int j = 0; j < k; ++j) {
+            double p = (double)w[j] * orc_bf16_to_f64(y[(int64_t)j * d + c]);
+            acc += p;
+            sa += fabs(p);
+        }
+        if (ysh) {
+            double p = sg * orc_bf16_to_f64(ysh[c]);
+            acc += p;
+            sa += fabs(p);
+        }
+        out[c] = acc;
+        if (s) s[c] = sa;
+    }
+}
+
+/* Batched O8 over n tokens (parity tests): w [n][k], y [n][k][d], ysh [n][d]
+ * (or NULL), sg [n] (or NULL = weight 1) -> out [n][d], s [n][d] (optional). */
+void orc_stage_combine(int n, int d, int k, const float *w, const uint16_t *y, const uint16_t *ysh,
+                       const float *sg, double *out, double *s) {
+    for (int t = 0; t < n; ++t)
+        orc_combine_f64(d, k, w + (int64_t)t * k, y + (int64_t)t * k * d, ysh ? ysh + (int64_t)t * d : NULL,
+                        sg ? (double)sg[t] : 1.0, out + (int64_t)t * d, s ? s + (int64_t)t * d : NULL);
+}
+
 /* O7' shared-expert gate (NEXT-3b: Qwen1.5-MoE shared_expert_gate, DESIGN.md
  *     R#17 variant): g_t = fp32( sum_i x[t][i] wsg[i] ) accumulated in fp64,
  *     s_t = fp32( 1 / (1 + exp(-g_t)) ) in fp64; the shared expert's output is
@@ -305,31 +409,26 @@ void orc_shared_gate(const uint16_t *x, const uint16_t *wsg, int T, int d, float
     }
 }
 
-int orc_moe_tokens2(int d, int E, int k, int F, int F_sh,
+/* O6-O8 for a list of tokens.
+ *   For token t (global index tokens[n]) and its k selected experts idx[t][j]
+ *   with weights w[t][j]:  y_j = FFN_{e_j}(x_t)  (O6);  y_sh = FFN_sh(x_t) if
+ *   F_sh > 0 (O7, R#16: shared expert added with weight 1, or sgate[t], O7');
+ *   out[n][c] = bf16( sum_j w_j * y_j[c]  (+ y_sh[c]) )   in fp64, j order
+ *   (O8, P:267 "aggregated via a weighted sum using the gating weights").
+ *   The FFN of a pair depends only on (x_t, expert weights): which EW or
+ *   slot serves it never enters (P:918 §5.1, stateless replay).
+ * w1/w3/w2: arrays of E pointers to the per-expert matrices.
+ * sgate (optional, [T] fp32): weight of the shared expert per token; NULL = 1.
+ * y_out (optional): [n_tokens][k][d] bf16 per-pair expert outputs.
+ * ysh_out (optional): [n_tokens][d] bf16 shared-expert outputs.
+ * out_f64 (optional): [n_tokens][d] out before its bf16 rounding (O8 exact).
+ * n_threads > 1 parallelises over tokens only (arithmetic per token unchanged). */
+int orc_moe_tokens3(int d, int E, int k, int F, int F_sh,
                     const uint16_t *x, const int32_t *idx, const float *w,
                     const uint16_t *const *w1, const uint16_t *const *w3, const uint16_t *const *w2,
                     const uint16_t *w1s, const uint16_t *w3s, const uint16_t *w2s, const float *sgate,
                     const int32_t *tokens, int n_tokens, uint16_t *out, uint16_t *y_out,
-                    int n_threads, uint16_t *ysh_out);
-
-int orc_moe_tokens(int d, int E, int k, int F, int F_sh,
-                   const uint16_t *x, const int32_t *idx, const float *w,
-                   const uint16_t *const *w1, const uint16_t *const *w3, const uint16_t *const *w2,
-                   const uint16_t *w1s, const uint16_t *w3s, const uint16_t *w2s,
-                   const int32_t *tokens, int n_tokens, uint16_t *out, uint16_t *y_out,
-                   int n_threads) {
-    return orc_moe_tokens2(d, E, k, F, F_sh, x, idx, w, w1, w3, w2, w1s, w3s, w2s, NULL, tokens, n_tokens,
-                           out, y_out, n_threads, NULL);
-}
-
-/* sgate (optional, [T] fp32): weight of the shared expert per token (O7'); NULL = 1.
- * ysh_out (optional, [n_tokens][d] bf16): the shared expert's output y_sh. */
-int orc_moe_tokens2(int d, int E, int k, int F, int F_sh,
-                    const uint16_t *x, const int32_t *idx, const float *w,
-                    const uint16_t *const *w1, const uint16_t *const *w3, const uint16_t *const *w2,
-                    const uint16_t *w1s, const uint16_t *w3s, const uint16_t *w2s, const float *sgate,
-                    const int32_t *tokens, int n_tokens, uint16_t *out, uint16_t *y_out,
-                    int n_threads, uint16_t *ysh_out) {
+                    int n_threads, uint16_t *ysh_out, double *out_f64) {
     if (k < 1 || k > E || d < 1 || F < 1) return ORC_ERR_INVALID;
     int Fmax = F > F_sh ? F : F_sh;
     int bad = 0;
@@ -338,32 +437,52 @@ int orc_moe_tokens2(int d, int E, int k, int F, int F_sh,
 #pragma omp parallel for schedule(dynamic, 1) num_threads(n_threads)
 #endif
     for (int n = 0; n < n_tokens; ++n) {
-        double *hbuf = (double *)malloc(sizeof(double) * (size_t)Fmax);
+        double *hwork = (double *)malloc(sizeof(double) * (size_t)Fmax);
+        uint16_t *hbf = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)Fmax);
+        double *work = (double *)malloc(sizeof(double) * (size_t)d);
         uint16_t *y = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)d * (k + 1));
         int t = tokens ? tokens[n] : n;
         const uint16_t *xt = x + (int64_t)t * d;
         for (int j = 0; j < k; ++j) {
             int e = idx[(int64_t)t * k + j];
             if (e < 0 || e >= E) { bad = 1; continue; }
-            orc_ffn(xt, d, F, w1[e], w3[e], w2[e], hbuf, y + (int64_t)j * d);
+            orc_ffn(xt, d, F, w1[e], w3[e], w2[e], hwork, hbf, work, y + (int64_t)j * d);
             if (y_out) memcpy(y_out + ((int64_t)n * k + j) * d, y + (int64_t)j * d, sizeof(uint16_t) * d);
         }
         if (F_sh > 0) {
-            orc_ffn(xt, d, F_sh, w1s, w3s, w2s, hbuf, y + (int64_t)k * d);
+            orc_ffn(xt, d, F_sh, w1s, w3s, w2s, hwork, hbf, work, y + (int64_t)k * d);
             if (ysh_out) memcpy(ysh_out + (int64_t)n * d, y + (int64_t)k * d, sizeof(uint16_t) * d);
         }
-        for (int c = 0; c < d; ++c) {
-            double acc = 0.0;
-            for (int j = 0; j < k; ++j)
-                acc += (double)w[(int64_t)t * k + j] * orc_bf16_to_f64(y[(int64_t)j * d + c]);
-            if (F_sh > 0)
-                acc += (sgate ? (double)sgate[t] : 1.0) * orc_bf16_to_f64(y[(int64_t)k * d + c]);
-            out[(int64_t)n * d + c] = orc_bf16_from_f64(acc);
-        }
-        free(hbuf);
+        orc_combine_f64(d, k, w + (int64_t)t * k, y, F_sh > 0 ? y + (int64_t)k * d : NULL,
+                        sgate ? (double)sgate[t] : 1.0, work, NULL);
+        for (int c = 0; c < d; ++c) out[(int64_t)n * d + c] = orc_bf16_from_f64(work[c]);
+        if (out_f64) memcpy(out_f64 + (int64_t)n * d, work, sizeof(double) * d);
+        free(hwork);
+        free(hbf);
+        free(work);
         free(y);
     }
     return bad ? ORC_ERR_INVALID : ORC_OK;
+}
+
+int orc_moe_tokens2(int d, int E, int k, int F, int F_sh,
+                    const uint16_t *x, const int32_t *idx, const float *w,
+                    const uint16_t *const *w1, const uint16_t *const *w3, const uint16_t *const *w2,
+                    const uint16_t *w1s, const uint16_t *w3s, const uint16_t *w2s, const float *sgate,
+                    const int32_t *tokens, int n_tokens, uint16_t *out, uint16_t *y_out,
+                    int n_threads, uint16_t *ysh_out) {
+    return orc_moe_tokens3(d, E, k, F, F_sh, x, idx, w, w1, w3, w2, w1s, w3s, w2s, sgate, tokens, n_tokens,
+                           out, y_out, n_threads, ysh_out, NULL);
+}
+
+int orc_moe_tokens(int d, int E, int k, int F, int F_sh,
+                   const uint16_t *x, const int32_t *idx, const float *w,
+                   const uint16_t *const *w1, const uint16_t *const *w3, const uint16_t *const *w2,
+                   const uint16_t *w1s, const uint16_t *w3s, const uint16_t *w2s,
+                   const int32_t *tokens, int n_tokens, uint16_t *out, uint16_t *y_out,
+                   int n_threads) {
+    return orc_moe_tokens3(d, E, k, F, F_sh, x, idx, w, w1, w3, w2, w1s, w3s, w2s, NULL, tokens, n_tokens,
+                           out, y_out, n_threads, NULL, NULL);
 }
 
 int orc_version(void) { return 1; }

@@ -389,3 +389,70 @@ def test_v_size_law_mixtral():
     """App. C: V = 2 * Top_k * N_hidden * S_elem = 32768 B for Mixtral bf16."""
     sh = wl.CONFIGS["mixtral_decode"]
     assert 2 * sh.k * sh.d * 2 == 32768
+
+
+# ---------------------------------------------------------------- unrounded stage values (R#21)
+
+def test_k_equals_E_has_no_near_tie():
+    """O2 with k == E: there is no (k+1)-th logit, so gap = +inf (no token is a near tie)."""
+    l = np.zeros((3, 4), np.float32)
+    _, _, gap = oracle.select(l, 4)
+    assert np.all(np.isinf(gap)) and np.all(gap > 0)
+
+
+def test_router_f64_vs_torch_fp64():
+    """O1 before rounding == torch fp64 x @ Wg^T; its fp32 rounding is O1; s = |x| @ |Wg|^T."""
+    g = torch.Generator().manual_seed(61)
+    x = torch.randn(40, 128, generator=g).to(torch.bfloat16)
+    wg = (torch.randn(12, 128, generator=g) * 0.1).to(torch.bfloat16)
+    l, s = oracle.router_f64(wl.as_u16(x), wl.as_u16(wg))
+    ref = (x.double() @ wg.double().T).numpy()
+    np.testing.assert_allclose(l, ref, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(s, (x.double().abs() @ wg.double().abs().T).numpy(), rtol=1e-13)
+    np.testing.assert_array_equal(l.astype(np.float32), oracle.router(wl.as_u16(x), wl.as_u16(wg)))
+
+
+def test_stage_h_and_y_vs_torch_fp64():
+    """O6a / O6b unrounded values == torch fp64 SwiGLU halves (silu(x W1^T) * x W3^T, then h W2^T)."""
+    d, F, n = 96, 160, 24
+    w1, w3, w2 = _rand_expert(d, F, 62)
+    x = torch.randn(n, d, generator=torch.Generator().manual_seed(63)).to(torch.bfloat16)
+    st = oracle.stage_h(wl.as_u16(x), wl.as_u16(w1), wl.as_u16(w3), n_threads=2)
+    xd = x.double()
+    a1, a3 = xd @ w1.double().T, xd @ w3.double().T
+    np.testing.assert_allclose(st["a1"], a1.numpy(), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(st["a3"], a3.numpy(), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(st["h"], (Fn.silu(a1) * a3).numpy(), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(st["s1"], (xd.abs() @ w1.double().abs().T).numpy(), rtol=1e-12)
+    hb = bf16_rne_exact(st["h"])
+    y, s = oracle.stage_y(hb, wl.as_u16(w2), n_threads=2)
+    hd = torch.from_numpy(bf16_bits_to_f64(hb))
+    np.testing.assert_allclose(y, (hd @ w2.double().T).numpy(), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(s, (hd.abs() @ w2.double().abs().T).numpy(), rtol=1e-12)
+    # the stages rounded at the R#7 storage points are exactly O6 (the oracle's y)
+    np.testing.assert_array_equal(bf16_rne_exact(y), _torch_swiglu_bf16(x, w1, w3, w2))
+
+
+def test_stage_combine_and_out_f64():
+    """O8 before rounding: out_f64 = sum_j w_j y_j (+ sg y_sh) in fp64 (numpy), its RNE is the
+    oracle's out; closed form k = 1, w = 1 -> out_f64 == y exactly."""
+    sh = wl.CONFIGS["tiny"]
+    L = wl.make_layer(sh, seed=1007)
+    x = wl.make_tokens(sh, seed=1007, T=64)
+    pl = wl.make_placement(sh.E, 2, 1)
+    args = ([wl.as_u16(a) for a in L.w1], [wl.as_u16(a) for a in L.w3], [wl.as_u16(a) for a in L.w2])
+    r = oracle.layer(wl.as_u16(x), wl.as_u16(L.wg), sh.k, *args, pl.cand, pl.ew_rank, pl.slots_per_ew,
+                     np.zeros(2, np.uint8), G=1, want_y=True)
+    yv = bf16_bits_to_f64(r["y"])
+    ref = np.sum(r["w"].astype(np.float64)[:, :, None] * yv, axis=1)
+    np.testing.assert_allclose(r["out_f64"], ref, rtol=1e-15, atol=0)
+    np.testing.assert_array_equal(bf16_rne_exact(r["out_f64"]), r["out"])
+    o, s = oracle.stage_combine(r["w"], r["y"])
+    np.testing.assert_array_equal(o, r["out_f64"])
+    np.testing.assert_allclose(s, np.sum(np.abs(r["w"].astype(np.float64)[:, :, None] * yv), axis=1), rtol=1e-15)
+    one = np.ones((64, 1), np.float32)
+    o1, _ = oracle.stage_combine(one, r["y"][:, :1])
+    np.testing.assert_array_equal(o1, yv[:, 0])
+    sg = np.full(64, 0.25, np.float32)
+    o2, _ = oracle.stage_combine(one, r["y"][:, :1], ysh=r["y"][:, 1], sg=sg)
+    np.testing.assert_array_equal(o2, yv[:, 0] + 0.25 * yv[:, 1])
