@@ -89,16 +89,35 @@ typedef struct {
  * config before tg_connect_peers().                                      */
 tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg_ctx **out);
 
-/* Peer bootstrap (world > 1).  tg_peer_handle_size() bytes per rank: the
- * caller gathers every rank's handle (e.g. torch.distributed.all_gather) and
- * passes them concatenated in rank order to tg_connect_peers(), which maps
- * each peer's buffers for direct NVLink loads/stores.  world == 1 needs no
- * connect call.                                                           */
+/* Peer bootstrap (world > 1; point-to-point, no collective
+ * group per call).  tg_peer_handle_size() bytes per rank: the caller gathers
+ * every rank's handle (e.g. torch.distributed.all_gather) and passes them
+ * concatenated in rank order to tg_connect_peers(), which maps each peer's
+ * buffers for direct NVLink loads/stores.  A handle carries the layout
+ * signature of the rank's peer-visible region (one-sided stores land at the
+ * sender's offsets): every rank must use the same tg_config, including
+ * max_tokens_per_rank, else TG_ERR_PEER and nothing is mapped.  world == 1
+ * needs no connect call.                                                   */
 size_t tg_peer_handle_size(void);
 tg_status tg_get_peer_handle(tg_ctx *ctx, void *out);
 tg_status tg_connect_peers(tg_ctx *ctx, const void *all_handles);
 
-/* Router weights Wg [E][d] bf16 (host or device source; copied).  SPMD.   */
+/* Virtual ranks on one GPU (tests, and a GPU shared by several AW/EW
+ * shards): ctxs[q] (q < world) are the ctxs of ranks 0..world-1, created in
+ * this process on the SAME device; tg_connect_local(ctx, ctxs) maps them as
+ * ctx's peers by device pointer (the data plane is the same code as over
+ * NVLink: stores into peer regions, epoch flags).  Layout signatures must
+ * match (TG_ERR_PEER).  tg_set_launch_ctas(ctx, n) (before the first call)
+ * sets the CTAs of each launch: 0 = one per SM (default, cooperative launch);
+ * 0 < n < SM count = a share of the GPU — the ranks' calls must then be
+ * enqueued on different streams and their shares must add up to at most the
+ * SM count, so that every rank's grid is resident at once.                */
+tg_status tg_connect_local(tg_ctx *ctx, tg_ctx *const *ctxs);
+tg_status tg_set_launch_ctas(tg_ctx *ctx, int n_ctas);
+
+/* Router weights Wg [E][d] bf16 (host or device source; copied).  SPMD.
+ * The gating network of P:265 §2.1 ("a gating network ... selects the top-k
+ * experts"): a linear router without bias (R#1).                 */
 tg_status tg_load_gate(tg_ctx *ctx, const void *wg, int src_on_device);
 
 /* Load expert `expert_id` into slot `slot` of EW `ew` (P:954 shadow experts:
@@ -110,11 +129,14 @@ tg_status tg_load_experts(tg_ctx *ctx, int ew, int slot, int expert_id, const vo
                           const void *w3, const void *w2, int src_on_device);
 
 /* Merged shared expert (F_sh = d_ffn_shared): w1, w3 [F_sh][d]; w2 [d][F_sh].
- * Replicated on every rank; added to the routed sum with weight 1.        */
+ * Replicated on every rank; added to the routed sum with weight 1.  Not in
+ * the paper: BASELINE.json configs[3] (DeepSeek-V2-Lite shape, "+ 2 shared");
+ * DESIGN.md R#16.                                                          */
 tg_status tg_load_shared(tg_ctx *ctx, const void *w1, const void *w3, const void *w2,
                          int src_on_device);
 
-/* Shared-expert gate vector wsg [d] bf16 (config shared_gate = 1).  SPMD.   */
+/* Shared-expert gate vector wsg [d] bf16 (config shared_gate = 1).  SPMD.
+ * Not in the paper: the public Qwen1.5-MoE shared_expert_gate, R#17. */
 tg_status tg_load_shared_gate(tg_ctx *ctx, const void *wsg, int src_on_device);
 
 /* Expert Routing Table (§4.2): cand[e][c] = (ew, slot) for
@@ -157,13 +179,22 @@ tg_status tg_mask_rank(tg_ctx *ctx, int rank, int masked);
  * recomputes them and `out` for every token, all within the same call's inputs
  * (x, n_tokens must be the failed call's; outputs of pairs other EWs served are
  * kept) — bitwise the output an unfailed call gives.  *failed = bit mask of the
- * failed ranks (0: nothing to do, out untouched).  Returns TG_OK, or
- * TG_ERR_NO_ROUTE when some re-routed pair's next live candidate is on another
- * rank (not recomputed in this call; the mask is applied for the next call).
- * Scope: fail-stop peers that failed after the count exchange of the call (a
- * peer that never publishes its counts stalls the exchange: device error, as
- * before); other survivors must also mask the failed rank before their next
- * call (tg_failover or tg_mask_rank).                                       */
+ * failed ranks (0: nothing to do, out untouched).
+ * Detection: within a call every live rank waits for every other live rank's
+ * count flag (timeout 10 x the failure timeout, <= 4 s: host threads may be
+ * late) and combine flag, so all survivors see a rank that fails at any point
+ * of the call in that same call; a rank silent in the count exchange is taken
+ * as failed with zero rows (EWs proceed with the tokens they have, §5.2
+ * P:927-941) and nothing is dispatched to it.
+ * Replay: tg_failover is collective among the survivors (every surviving rank
+ * calls it after every call; it returns at once when nothing failed).  The
+ * re-routed pairs go to the next live candidate of their expert on WHICHEVER
+ * rank it lives (a replay run with its own flags: the replay rows are the
+ * whole work list of the EWs that serve them, "replayed requests are
+ * prioritized").  Returns TG_OK; TG_ERR_NO_ROUTE when some pair has no live
+ * candidate left (not recomputed); TG_ERR_PEER when another rank failed
+ * during the replay itself (call tg_failover again).  No device wait on a
+ * peer traps: a silent peer is always recorded as failed.                   */
 tg_status tg_set_failure_timeout(tg_ctx *ctx, double ms);
 tg_status tg_failover(tg_ctx *ctx, const void *x, void *out, int n_tokens, void *stream, uint32_t *failed);
 
@@ -187,7 +218,10 @@ tg_status tg_inject_failure(tg_ctx *ctx);
  * tg_kv_committed(ctx, &seq): last committed seq (0: none yet).
  * tg_kv_restore(ctx, dst, bytes, offset, stream): waits for the pending
  * checkpoints, then copies bucket + offset back to DEVICE `dst` on `stream`
- * (request-level restoration).  Errors: TG_ERR_NOT_LOADED (no
+ * (request-level restoration).  `seg` must stay allocated and
+ * unmodified until tg_kv_committed() reaches seq (the copy runs later, on
+ * the checkpoint stream; the Python binding keeps a reference until then).
+ * Errors: TG_ERR_NOT_LOADED (no
  * store), TG_ERR_INVALID (range), TG_ERR_STALE_VERSION (seq not increasing),
  * TG_ERR_UNSUPPORTED (host-only ctx), TG_ERR_OOM.                          */
 tg_status tg_kv_store_init(tg_ctx *ctx, size_t bytes);
@@ -217,17 +251,42 @@ tg_status tg_moe_layer_host(tg_ctx *ctx, const void *x_host, void *out_host, int
 /* Routing of the LAST call, for parity tests (device destination buffers,
  * any may be NULL):  idx int32 [n][k] (ascending expert id), w fp32 [n][k],
  * dst_rank / dst_slot (bank slot on that rank) / dst_pos (row in that rank's
- * receive buffer) int32 [n][k], counts int32 [world][S_max] = rows per
- * (rank, bank slot) summed over ALL source ranks.  Enqueued on stream.      */
-tg_status tg_get_routing(tg_ctx *ctx, int32_t *idx, float *w, int32_t *dst_rank,
+ * receive buffer; -1 for a pair whose destination failed in the count
+ * exchange) int32 [n][k], counts int32 [world][S_max] = rows per (rank, bank
+ * slot) summed over ALL source ranks.  n_tokens must equal the last call's
+ * (TG_ERR_INVALID otherwise: the buffers are sized by it).  Enqueued on
+ * stream.                                                                  */
+tg_status tg_get_routing(tg_ctx *ctx, int n_tokens, int32_t *idx, float *w, int32_t *dst_rank,
                          int32_t *dst_slot, int32_t *dst_pos, int32_t *counts, void *stream);
+
+/* Stage values of the LAST call on this rank, for per-storage-point parity
+ * tests: each is what the next stage of the path read.
+ *   TG_STAGE_LOGITS fp32 [n][E (+1 shared-gate row)]  router logits O1 (only
+ *                   written while tg_set_stage_export(ctx, 1) is on)
+ *   TG_STAGE_RECV   bf16 [R][d]   token rows this EW received (R = rows of all
+ *                   its slots, slots in ascending bank slot, P:385 batches)
+ *   TG_STAGE_META   int32 [R][2]  origin of each row: (source rank, t * k + j)
+ *   TG_STAGE_H      bf16 [R][F]   SwiGLU activations h = silu(a1) * a3 (O6a)
+ *   TG_STAGE_Y      bf16 [n][k][d] expert outputs returned to this AW (O6b)
+ *   TG_STAGE_HSH / TG_STAGE_YSH  bf16 [n][F_sh] / [n][d]  shared expert (O7)
+ *   TG_STAGE_SGATE  fp32 [n]      sigmoid shared-expert gate (O7')
+ * tg_get_stage(ctx, stage, dst, cap, &bytes) synchronises the device and
+ * copies `bytes` to dst (host or device; dst = NULL: size query only).
+ * TG_ERR_INVALID if cap < bytes or the stage is unknown.                    */
+enum { TG_STAGE_LOGITS = 0, TG_STAGE_RECV = 1, TG_STAGE_META = 2, TG_STAGE_H = 3, TG_STAGE_Y = 4,
+       TG_STAGE_HSH = 5, TG_STAGE_YSH = 6, TG_STAGE_SGATE = 7 };
+tg_status tg_set_stage_export(tg_ctx *ctx, int on);
+tg_status tg_get_stage(tg_ctx *ctx, int stage, void *dst, size_t cap, size_t *bytes);
 
 /* S_max = max bank slots on any rank; bank slot of (ew, slot) on its rank. */
 int tg_max_slots(const tg_ctx *ctx);
 int tg_bank_slot(const tg_ctx *ctx, int ew, int slot);
 
 /* Cumulative rows routed to each (rank, bank slot) since tg_init, from this
- * rank's tokens: int64 [world][S_max] host array.  Synchronises the device. */
+ * rank's tokens: int64 [world][S_max] host array.  Synchronises the device.
+ * The per-EW load the paper's shadow-inactivity and failover experiments
+ * observe (App. D: shadows receive no traffic until activated;
+ * §5.1: a masked EW receives none after the reroute).            */
 tg_status tg_get_stats(tg_ctx *ctx, int64_t *rows);
 
 /* Per-kernel CUDA-event timing (events on the call's stream around each

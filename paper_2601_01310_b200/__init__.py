@@ -47,6 +47,10 @@ _SIG = {
     "tg_peer_handle_size": ([], ctypes.c_size_t),
     "tg_get_peer_handle": ([_P, _P], _I),
     "tg_connect_peers": ([_P, _P], _I),
+    "tg_connect_local": ([_P, _P], _I),
+    "tg_set_launch_ctas": ([_P, _I], _I),
+    "tg_set_stage_export": ([_P, _I], _I),
+    "tg_get_stage": ([_P, _I, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)], _I),
     "tg_load_gate": ([_P, _P, _I], _I),
     "tg_load_experts": ([_P, _I, _I, _I, _P, _P, _P, _I], _I),
     "tg_load_shared": ([_P, _P, _P, _P, _I], _I),
@@ -64,7 +68,7 @@ _SIG = {
     "tg_moe_layer": ([_P, _P, _P, _I, _P], _I),
     "tg_moe_layer_host": ([_P, _P, _P, _I, _P], _I),
     "tg_host_sync": ([_P, _P], _I),
-    "tg_get_routing": ([_P, _P, _P, _P, _P, _P, _P, _P], _I),
+    "tg_get_routing": ([_P, _I, _P, _P, _P, _P, _P, _P, _P], _I),
     "tg_max_slots": ([_P], _I),
     "tg_bank_slot": ([_P, _I, _I], _I),
     "tg_get_stats": ([_P, _P], _I),
@@ -81,6 +85,9 @@ for _n, (_a, _r) in _SIG.items():
     _f.argtypes, _f.restype = _a, _r
 
 EXPORTED = tuple(_SIG)
+
+TG_STAGE_LOGITS, TG_STAGE_RECV, TG_STAGE_META, TG_STAGE_H, TG_STAGE_Y = 0, 1, 2, 3, 4
+TG_STAGE_HSH, TG_STAGE_YSH, TG_STAGE_SGATE = 5, 6, 7
 
 
 class TarragonError(RuntimeError):
@@ -147,6 +154,35 @@ def tg_connect_peers(ctx, handles: bytes):
     _check(ctx, _lib.tg_connect_peers(ctx, handles), "tg_connect_peers")
 
 
+def tg_connect_local(ctx, ctxs):
+    """Map the ctxs of every rank (same process, same device) as ctx's peers."""
+    arr = (_P * len(ctxs))(*[c.value if isinstance(c, _P) else c for c in ctxs])
+    _check(ctx, _lib.tg_connect_local(ctx, arr), "tg_connect_local")
+
+
+def tg_set_launch_ctas(ctx, n: int):
+    _check(ctx, _lib.tg_set_launch_ctas(ctx, int(n)), "tg_set_launch_ctas")
+
+
+def tg_set_stage_export(ctx, on=True):
+    _check(ctx, _lib.tg_set_stage_export(ctx, int(on)), "tg_set_stage_export")
+
+
+_STAGE_DTYPE = {0: np.float32, 1: np.uint16, 2: np.int32, 3: np.uint16, 4: np.uint16, 5: np.uint16, 6: np.uint16,
+                7: np.float32}
+
+
+def tg_get_stage(ctx, stage: int) -> np.ndarray:
+    """Flat host copy of a stage value of the last call (see include/tarragon.h)."""
+    n = ctypes.c_size_t(0)
+    _check(ctx, _lib.tg_get_stage(ctx, stage, None, 0, ctypes.byref(n)), "tg_get_stage")
+    dt = np.dtype(_STAGE_DTYPE[stage])
+    buf = np.empty(n.value // dt.itemsize, dt)
+    if n.value:
+        _check(ctx, _lib.tg_get_stage(ctx, stage, buf.ctypes.data, n.value, ctypes.byref(n)), "tg_get_stage")
+    return buf
+
+
 def tg_load_gate(ctx, wg: torch.Tensor):
     _check(ctx, _lib.tg_load_gate(ctx, _ptr(wg), int(wg.is_cuda)), "tg_load_gate")
 
@@ -204,11 +240,22 @@ def tg_kv_store_init(ctx, nbytes: int) -> int:
     return _check(ctx, _lib.tg_kv_store_init(ctx, int(nbytes)), "tg_kv_store_init")
 
 
+_KV_PENDING = {}  # ctx -> [(seq, tensor)]: segments kept alive until their commit record
+
+
 def tg_kv_checkpoint(ctx, seg: torch.Tensor, offset: int, seq: int, stream=None) -> int:
-    """Checkpoint the device tensor `seg` (contiguous) at bucket offset `offset` with sequence number seq."""
+    """Checkpoint the device tensor `seg` (contiguous) at bucket offset `offset` with sequence number seq.
+    A reference to `seg` is kept until seq is committed (the copy runs later on the checkpoint stream);
+    the caller must not modify `seg` before tg_kv_committed() >= seq."""
     nbytes = seg.numel() * seg.element_size()
-    return _check(ctx, _lib.tg_kv_checkpoint(ctx, _ptr(seg), nbytes, int(offset), int(seq), _stream(stream)),
-                  "tg_kv_checkpoint")
+    rc = _check(ctx, _lib.tg_kv_checkpoint(ctx, _ptr(seg), nbytes, int(offset), int(seq), _stream(stream)),
+                "tg_kv_checkpoint")
+    key = ctx.value if isinstance(ctx, _P) else ctx
+    done = tg_kv_committed(ctx)
+    pend = [(q, t) for q, t in _KV_PENDING.get(key, []) if q > done]
+    pend.append((int(seq), seg))
+    _KV_PENDING[key] = pend
+    return rc
 
 
 def tg_kv_committed(ctx) -> int:
@@ -237,14 +284,15 @@ def tg_moe_layer_host(ctx, x_host: torch.Tensor, out_host: torch.Tensor, stream=
 
 
 def tg_get_routing(ctx, n_tokens, k, world, S_max, device, stream=None):
+    """Routing of the last call (n_tokens must be that call's token count)."""
     idx = torch.empty(n_tokens, k, dtype=torch.int32, device=device)
     w = torch.empty(n_tokens, k, dtype=torch.float32, device=device)
     dr = torch.empty(n_tokens, k, dtype=torch.int32, device=device)
     ds = torch.empty(n_tokens, k, dtype=torch.int32, device=device)
     dp = torch.empty(n_tokens, k, dtype=torch.int32, device=device)
     counts = torch.empty(world, S_max, dtype=torch.int32, device=device)
-    _check(ctx, _lib.tg_get_routing(ctx, _ptr(idx), _ptr(w), _ptr(dr), _ptr(ds), _ptr(dp), _ptr(counts),
-                                    _stream(stream)), "tg_get_routing")
+    _check(ctx, _lib.tg_get_routing(ctx, int(n_tokens), _ptr(idx), _ptr(w), _ptr(dr), _ptr(ds), _ptr(dp),
+                                    _ptr(counts), _stream(stream)), "tg_get_routing")
     return dict(idx=idx, w=w, dst_rank=dr, dst_slot=ds, dst_pos=dp, counts=counts)
 
 
@@ -302,6 +350,7 @@ def tg_last_launch_count(ctx) -> int:
 
 def tg_finalize(ctx):
     if ctx:
+        _KV_PENDING.pop(ctx.value if isinstance(ctx, _P) else ctx, None)
         _lib.tg_finalize(ctx)
 
 
@@ -317,19 +366,28 @@ class MoELayer:
     (see workloads.make_placement).  weights: object with wg, w1, w3, w2 lists
     (torch bf16, host or device) and optional shared = (w1s, w3s, w2s).
     For world > 1 pass an initialised torch.distributed process group: the
-    peer handles are all-gathered through it.
+    peer handles are all-gathered through it.  ``local_ranks`` builds the
+    ranks of a world as virtual ranks on one GPU instead (see that function).
     """
 
     def __init__(self, shape, placement, weights, max_tokens_per_rank, rank=0, world=1, device=None,
-                 group=None, version=1):
+                 group=None, version=1, _peers=None, launch_ctas=0):
         self.shape, self.pl = shape, placement
         self.rank, self.world = rank, world
+        self.stage_export = False
         self.device = torch.cuda.current_device() if device is None else device
         self.ctx = tg_init(shape.d, shape.E, shape.k, shape.F, placement.n_ews, placement.ew_rank,
                            placement.slots_per_ew, max_tokens_per_rank, rank, world, self.device,
                            d_ffn_shared=shape.F_sh, gate_mode=getattr(shape, "gate_mode", 0),
                            shared_gate=getattr(shape, "shared_gate", 0))
-        if world > 1:
+        if launch_ctas:
+            tg_set_launch_ctas(self.ctx, launch_ctas)
+        if _peers is not None:
+            _peers.append(self.ctx)
+            if len(_peers) == world:  # the last virtual rank connects everyone
+                for c in _peers:
+                    tg_connect_local(c, _peers)
+        elif world > 1:
             import torch.distributed as dist
             h = tg_get_peer_handle(self.ctx)
             t = torch.frombuffer(bytearray(h), dtype=torch.uint8).to(f"cuda:{self.device}")
@@ -381,6 +439,14 @@ class MoELayer:
         _check(self.ctx, rc, "tg_moe_layer")
         return out
 
+    def stage(self, which: int) -> np.ndarray:
+        return tg_get_stage(self.ctx, which)
+
+    def export_stages(self, on=True):
+        """Parity tests: also export the router logits of each call (TG_STAGE_LOGITS)."""
+        tg_set_stage_export(self.ctx, on)
+        self.stage_export = bool(on)
+
     def routing(self, n_tokens, stream=None):
         return tg_get_routing(self.ctx, n_tokens, self.shape.k, self.world, self.S_max,
                               f"cuda:{self.device}", stream)
@@ -398,3 +464,34 @@ class MoELayer:
                 self.close()
         except Exception:
             pass
+
+
+def local_ranks(shape, placement, weights, max_tokens_per_rank, world, device=None, n_sms=None):
+    """``world`` virtual ranks of one layer on ONE GPU (tests / driver evidence of the
+    multi-rank data plane): ctxs connected by device pointer (tg_connect_local), each
+    launching on n_sms // world CTAs.  Their calls must be enqueued on different
+    streams (``call_all``)."""
+    device = torch.cuda.current_device() if device is None else device
+    n_sms = n_sms or torch.cuda.get_device_properties(device).multi_processor_count
+    peers = []
+    layers = [None] * world
+    # every ctx must exist before any is connected: create, then load (connect happens on the last init)
+    for r in range(world):
+        layers[r] = MoELayer(shape, placement, weights, max_tokens_per_rank, rank=r, world=world, device=device,
+                             _peers=peers, launch_ctas=n_sms // world)
+    return layers
+
+
+def call_all(layers, xs, outs=None, streams=None, skip=()):
+    """One tg_moe_layer call of every virtual rank (rank r on streams[r]); ranks in ``skip`` do
+    not call (a rank that died before the call).  Returns the statuses; does not synchronise."""
+    streams = streams or [torch.cuda.Stream() for _ in layers]
+    outs = outs or [torch.empty_like(x) for x in xs]
+    rcs = []
+    for r, (L, x, o, st) in enumerate(zip(layers, xs, outs, streams)):
+        if r in skip:
+            rcs.append(None)
+            continue
+        st.wait_stream(torch.cuda.current_stream())
+        rcs.append(tg_moe_layer(L.ctx, x, o, st))
+    return rcs, outs, streams

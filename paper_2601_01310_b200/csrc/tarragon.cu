@@ -68,6 +68,9 @@ struct tg_ctx {
   // ---- device
   bool host_only = true;
   int n_sms = 148;
+  int n_ctas = 0;                         // CTAs per launch (0 = one per SM); < n_sms: GPU shared by virtual ranks
+  bool stage_export = false;              // parity export of the router logits (tg_set_stage_export)
+  float *logits = nullptr;                // [T_max][E_r]
   bf16 *bank_w1 = nullptr, *bank_w3 = nullptr, *bank_w2 = nullptr, *wg = nullptr;
   bf16 *w1s = nullptr, *w3s = nullptr, *w2s = nullptr;
   uint8_t *sym = nullptr;                 // own symmetric region
@@ -88,8 +91,10 @@ struct tg_ctx {
   long long host_calls = 0;
   uint32_t epoch = 0;    // local kernel runs
   uint32_t xepoch = 0;   // calls (equal on every rank)
+  uint32_t rxepoch = 0;  // failover replays (equal on every surviving rank)
   int32_t *key_main = nullptr, *key_replay = nullptr;
   long long fail_timeout_ns = 200000000LL;  // in-call failure detection on data / combine flags
+  long long cnt_timeout_ns = 2000000000LL;  // count-exchange waits (10 x the failure timeout, <= 4 s)
   bool inject_next = false;                 // fault injection for tests (tg_inject_failure)
   // KV checkpoint store (NEXT-4): pinned host bucket written by the copy engines
   uint8_t *kv_bucket = nullptr;
@@ -213,8 +218,10 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   c->mask.assign(c->W, 0);
   c->rkey.assign(E, -1);
   // worst-case rows received by one rank: every token of every rank, at most
-  // min(k, S_loc) rows each (distinct experts -> distinct slots)
-  c->R_cap = world * c->T_max * std::min(k, std::max(c->S_loc, 1));
+  // min(k, S_max) rows each (distinct experts -> distinct slots).  Sized from global
+  // values only, so the peer-visible region has the same layout on every rank
+  // (checked at connect time): senders store into a peer at their own offsets.
+  c->R_cap = world * c->T_max * std::min(k, std::max(c->S_max, 1));
   c->R_sh0 = c->R_cap;
   c->R_tot = c->R_cap + (Fsh > 0 ? c->T_max : 0);
   // fixed split-K for long GEMM2 reductions: a function of the shape only
@@ -264,7 +271,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   L.meta = off; off = align_up(off + (size_t)c->R_tot * 8, 1024);
   L.dup = off; off = align_up(off + (size_t)c->R_tot * 4, 1024);
   L.ybuf = off; off = align_up(off + Tm * k * d * 2, 1024);
-  L.cnt_all = off; off = align_up(off + (size_t)2 * world * c->nkeys * 4, 1024);
+  L.cnt_all = off; off = align_up(off + (size_t)3 * world * c->nkeys * 4, 1024);
   L.flags = off; off = align_up(off + kNumFlagKinds * kMaxWorld * 4, 1024);
   L.total = off;
   CKI(cudaMalloc(&c->sym, L.total));
@@ -281,6 +288,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t so = 0;
   auto carve = [&](size_t bytes) { size_t o = so; so = align_up(so + bytes, 256); return o; };
   size_t o_sg = carve(Tm * 4);
+  size_t o_lg = carve(Tm * (size_t)(E + 1) * 4);
   size_t o_idx = carve(Tm * k * 4), o_w = carve(Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
   size_t o_key2 = carve(Tm * k * 4);
   size_t o_lp = carve(((Tm + 31) / 32) * (size_t)(d / 64) * 32 * (E + 1) * 4);  // groups * nkp * 32 * E floats (KP >= 64)
@@ -312,6 +320,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
     a.l2_prefetch_bytes = e ? atoll(e) : (long long)(prop.l2CacheSize * 0.6);
   }
   a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.sgate = (float *)(sb + o_sg);
+  c->logits = (float *)(sb + o_lg);
   a.gate_mode = c->gate_mode; a.shared_gate = c->shared_gate; a.E_r = E + c->shared_gate; a.key = (int32_t *)(sb + o_key);
   c->key_main = a.key; c->key_replay = (int32_t *)(sb + o_key2);
   a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.chunk_ctr = (int32_t *)(sb + o_cc); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
@@ -369,14 +378,31 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   return TG_OK;
 }
 
-size_t tg_peer_handle_size(void) { return sizeof(cudaIpcMemHandle_t); }
+// A peer handle carries the IPC handle of the rank's peer-visible region and the
+// signature of its layout: one-sided stores land at the SENDER's offsets, so every
+// rank's region must have the same layout (same config and max_tokens_per_rank).
+struct PeerHandle {
+  cudaIpcMemHandle_t ipc;
+  uint64_t sig[8];
+};
+
+static void layout_signature(const tg_ctx *c, uint64_t *sig) {
+  sig[0] = c->L.total; sig[1] = c->L.recv ^ (c->L.meta << 20); sig[2] = c->L.ybuf ^ (c->L.dup << 20);
+  sig[3] = c->L.cnt_all ^ (c->L.flags << 20); sig[4] = (uint64_t)c->R_cap; sig[5] = (uint64_t)c->T_max;
+  sig[6] = ((uint64_t)c->nkeys << 32) | (uint64_t)c->world;
+  sig[7] = ((uint64_t)c->d << 40) ^ ((uint64_t)c->k << 32) ^ ((uint64_t)c->E << 16) ^ (uint64_t)c->S_max;
+}
+
+size_t tg_peer_handle_size(void) { return sizeof(PeerHandle); }
 
 tg_status tg_get_peer_handle(tg_ctx *c, void *out) {
   if (!c || !out) return TG_ERR_INVALID;
   if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx has no device buffers");
   CK(cudaSetDevice(c->device));
-  cudaIpcMemHandle_t h;
-  CK(cudaIpcGetMemHandle(&h, c->sym));
+  PeerHandle h;
+  memset(&h, 0, sizeof h);
+  CK(cudaIpcGetMemHandle(&h.ipc, c->sym));
+  layout_signature(c, h.sig);
   memcpy(out, &h, sizeof h);
   return TG_OK;
 }
@@ -386,16 +412,52 @@ tg_status tg_connect_peers(tg_ctx *c, const void *all) {
   if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx has no device buffers");
   CK(cudaSetDevice(c->device));
   const uint8_t *p = reinterpret_cast<const uint8_t *>(all);
+  uint64_t mine[8];
+  layout_signature(c, mine);
+  for (int q = 0; q < c->world; ++q) {  // validate every handle before mapping any
+    PeerHandle h;
+    memcpy(&h, p + (size_t)q * sizeof h, sizeof h);
+    if (memcmp(h.sig, mine, sizeof mine) != 0)
+      return fail(c, TG_ERR_PEER, "rank %d's peer-visible region has another layout (config or "
+                  "max_tokens_per_rank differ between ranks)", q);
+  }
   for (int q = 0; q < c->world; ++q) {
     if (q == c->rank) continue;
-    cudaIpcMemHandle_t h;
+    PeerHandle h;
     memcpy(&h, p + (size_t)q * sizeof h, sizeof h);
     void *ptr = nullptr;
-    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h.ipc, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return fail(c, TG_ERR_PEER, "cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
     c->peer[q] = reinterpret_cast<uint8_t *>(ptr);
     c->peer_opened[q] = true;
   }
+  return TG_OK;
+}
+
+tg_status tg_connect_local(tg_ctx *c, tg_ctx *const *ctxs) {
+  if (!c || !ctxs) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx has no device buffers");
+  uint64_t mine[8], theirs[8];
+  layout_signature(c, mine);
+  for (int q = 0; q < c->world; ++q) {
+    const tg_ctx *o = ctxs[q];
+    if (!o || o->host_only) return fail(c, TG_ERR_INVALID, "ctxs[%d] is null or host-only", q);
+    if (o->rank != q || o->world != c->world) return fail(c, TG_ERR_INVALID, "ctxs[%d] is rank %d of %d", q, o->rank, o->world);
+    if (o->device != c->device) return fail(c, TG_ERR_INVALID, "ctxs[%d] is on device %d, not %d", q, o->device, c->device);
+    layout_signature(o, theirs);
+    if (memcmp(theirs, mine, sizeof mine) != 0)
+      return fail(c, TG_ERR_PEER, "rank %d's peer-visible region has another layout", q);
+  }
+  for (int q = 0; q < c->world; ++q) c->peer[q] = ctxs[q]->sym;
+  return TG_OK;
+}
+
+tg_status tg_set_launch_ctas(tg_ctx *c, int n) {
+  if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
+  if (n < 0 || n > c->n_sms) return fail(c, TG_ERR_INVALID, "launch CTAs %d not in [0, %d]", n, c->n_sms);
+  if (c->epoch != 0) return fail(c, TG_ERR_INVALID, "tg_set_launch_ctas must precede the first call");
+  c->n_ctas = (n == c->n_sms) ? 0 : n;
   return TG_OK;
 }
 
@@ -431,6 +493,13 @@ tg_status tg_load_experts(tg_ctx *c, int ew, int slot, int expert, const void *w
   if (!c) return TG_ERR_INVALID;
   if (ew < 0 || ew >= c->W || slot < 0 || slot >= c->spe || expert < 0 || expert >= c->E)
     return fail(c, TG_ERR_INVALID, "tg_load_experts: ew %d slot %d expert %d out of range", ew, slot, expert);
+  if (c->have_table) {  // a slot the active route table names for another expert stays as it is
+    for (int e = 0; e < c->E; ++e)
+      for (int j = 0; j < c->C; ++j)
+        if (e != expert && c->cand[(e * c->C + j) * 2] == ew && c->cand[(e * c->C + j) * 2 + 1] == slot)
+          return fail(c, TG_ERR_INVALID, "tg_load_experts: (ew %d, slot %d) serves expert %d in route table "
+                      "version %llu; install a table without it first", ew, slot, e, (unsigned long long)c->version);
+  }
   if (!c->host_only && c->ew_rank[ew] == c->rank) {
     if (!w1 || !w3 || !w2) return fail(c, TG_ERR_INVALID, "tg_load_experts: null weights for a local EW");
     const size_t b = (size_t)c->F * c->d * 2;
@@ -527,6 +596,52 @@ tg_status tg_mask_rank(tg_ctx *c, int r, int masked) {
   return TG_OK;
 }
 
+// ------------------------------------------------------------ stage export (parity tests)
+tg_status tg_set_stage_export(tg_ctx *c, int on) {
+  if (!c) return TG_ERR_INVALID;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
+  c->stage_export = on != 0;
+  return TG_OK;
+}
+
+tg_status tg_get_stage(tg_ctx *c, int stage, void *dst, size_t cap, size_t *bytes) {
+  if (!c || !bytes) return TG_ERR_INVALID;
+  *bytes = 0;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());
+  tg_status st = check_sticky(c);
+  if (st) return st;
+  const CallArgs &a = c->args;
+  const size_t T = (size_t)c->last_T;
+  size_t R = 0;
+  if (stage == TG_STAGE_RECV || stage == TG_STAGE_META || stage == TG_STAGE_H) {
+    std::vector<int32_t> rows(std::max(c->S_loc, 1), 0);
+    if (c->S_loc) CK(cudaMemcpy(rows.data(), a.slot_rows, sizeof(int32_t) * c->S_loc, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < c->S_loc; ++i) R += (size_t)rows[i];
+  }
+  const void *src = nullptr;
+  size_t n = 0;
+  switch (stage) {
+    case TG_STAGE_LOGITS:
+      if (!c->stage_export) return fail(c, TG_ERR_INVALID, "logits are exported only after tg_set_stage_export(ctx, 1)");
+      src = c->logits; n = T * (size_t)(c->E + c->shared_gate) * 4; break;
+    case TG_STAGE_RECV: src = c->sym + c->L.recv; n = R * c->d * 2; break;
+    case TG_STAGE_META: src = c->sym + c->L.meta; n = R * 8; break;
+    case TG_STAGE_H: src = a.H; n = R * c->F * 2; break;
+    case TG_STAGE_Y: src = c->sym + c->L.ybuf; n = T * c->k * c->d * 2; break;
+    case TG_STAGE_HSH: src = a.Hs; n = c->Fsh ? T * c->Fsh * 2 : 0; break;
+    case TG_STAGE_YSH: src = a.ysh; n = c->Fsh ? T * c->d * 2 : 0; break;
+    case TG_STAGE_SGATE: src = a.sgate; n = c->shared_gate ? T * 4 : 0; break;
+    default: return fail(c, TG_ERR_INVALID, "unknown stage %d", stage);
+  }
+  *bytes = n;
+  if (!dst || n == 0) return TG_OK;
+  if (cap < n) return fail(c, TG_ERR_INVALID, "stage %d needs %zu bytes, buffer has %zu", stage, n, cap);
+  CK(cudaMemcpy(dst, src, n, cudaMemcpyDefault));
+  return TG_OK;
+}
+
 int tg_max_slots(const tg_ctx *c) { return c ? c->S_max : -1; }
 int tg_bank_slot(const tg_ctx *c, int ew, int slot) {
   if (!c || ew < 0 || ew >= c->W || slot < 0 || slot >= c->spe) return -1;
@@ -562,7 +677,10 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
   a.alive = c->alive;
   a.fslot_data = FLAG_DATA;
   a.fslot_comb = FLAG_COMB;
+  a.fslot_cnt = FLAG_CNT;
   a.fail_timeout_ns = c->fail_timeout_ns;
+  a.cnt_timeout_ns = c->cnt_timeout_ns;
+  a.logits = c->stage_export ? c->logits : nullptr;
   a.replay = 0;
   a.failed = 0;
   a.key_old = nullptr;
@@ -594,11 +712,12 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   CallArgs a = call_args(c, T, x, out, &rk);
   a.xepoch = ++c->xepoch;
   a.fepoch = a.xepoch;
+  a.cnt_buf = (int)(a.xepoch & 1);
   a.inject_fail = c->inject_next ? 1 : 0;
   c->inject_next = false;
   c->n_ev = 0;
   rec(c, s);
-  CK(launch_layer(a, rk, c->maps, c->n_sms, s));
+  CK(launch_layer(a, rk, c->maps, c->n_ctas ? c->n_ctas : c->n_sms, c->n_ctas != 0, s));
   rec(c, s);
   if (c->prof) ++c->prof_calls;
   c->last_T = T;
@@ -610,6 +729,7 @@ tg_status tg_set_failure_timeout(tg_ctx *c, double ms) {
   if (!c) return TG_ERR_INVALID;
   if (!(ms > 0.0) || ms > 4000.0) return fail(c, TG_ERR_INVALID, "failure timeout %g ms not in (0, 4000]", ms);
   c->fail_timeout_ns = (long long)(ms * 1e6);
+  c->cnt_timeout_ns = std::min(10 * c->fail_timeout_ns, 4000000000LL);
   return TG_OK;
 }
 
@@ -629,7 +749,7 @@ tg_status tg_failover(tg_ctx *c, const void *x, void *out, int T, void *stream, 
   tg_status st = check_sticky(c);
   if (st) return st;
   volatile int *hw = reinterpret_cast<volatile int *>(c->err_host);
-  const uint32_t fm = static_cast<uint32_t>(hw[4]) & ~(1u << c->rank);
+  const uint32_t fm = static_cast<uint32_t>(hw[4]) & ~(1u << c->rank) & c->alive;
   if (!fm) return TG_OK;  // the last call saw no peer failure: nothing to do
   if (T != c->last_T) return fail(c, TG_ERR_INVALID, "failover needs the failed call's tokens (%d, got %d)", c->last_T, T);
   hw[4] = 0;
@@ -643,25 +763,33 @@ tg_status tg_failover(tg_ctx *c, const void *x, void *out, int T, void *stream, 
     }
   resolve(c);
   if (failed) *failed = fm;
-  // ... and the pairs this rank sent them are recomputed on the next live candidate
+  // ... and the pairs this rank had sent them are re-dispatched to the next live candidate
+  // of their expert, on whichever surviving rank it lives: a replay run of k_layer in which
+  // every survivor takes part (the survivors all saw the failure in the same call: each
+  // waits for every live rank's combine flag), with its own flags and count buffer
   RouteKeys rk;
   CallArgs a = call_args(c, T, x, out, &rk);
   a.xepoch = c->xepoch;
-  a.fepoch = a.epoch;
+  a.fepoch = ++c->rxepoch;
   a.fslot_data = FLAG_RDATA;
   a.fslot_comb = FLAG_RCOMB;
-  a.alive = 1u << c->rank;  // local by construction: no peer takes part
+  a.fslot_cnt = FLAG_RCNT;
+  a.cnt_buf = kCntBufReplay;
   a.replay = 1;
   a.failed = fm;
   a.key_old = c->key_main;
   a.key = c->key_replay;
-  CK(launch_layer(a, rk, c->maps, c->n_sms, s));
+  a.logits = nullptr;
+  CK(launch_layer(a, rk, c->maps, c->n_ctas ? c->n_ctas : c->n_sms, c->n_ctas != 0, s));
   CK(cudaStreamSynchronize(s));
   st = check_sticky(c);
   if (st) return st;
+  c->last_launches = 1;
   if (hw[5] > 0)
-    return fail(c, TG_ERR_NO_ROUTE, "%d pairs have their next live candidate on another rank: not recomputed "
-                "in this call (their tokens' outputs are incomplete)", hw[5]);
+    return fail(c, TG_ERR_NO_ROUTE, "%d pairs have no live candidate left: not recomputed (their tokens' "
+                "outputs are incomplete)", hw[5]);
+  if (static_cast<uint32_t>(hw[4]) & ~(1u << c->rank) & c->alive)
+    return fail(c, TG_ERR_PEER, "another rank failed during the replay (call tg_failover again)");
   return TG_OK;
 }
 
@@ -730,10 +858,12 @@ tg_status tg_host_sync(tg_ctx *c, void *stream) {
   return TG_OK;
 }
 
-tg_status tg_get_routing(tg_ctx *c, int32_t *idx, float *w, int32_t *dst_rank, int32_t *dst_slot, int32_t *dst_pos,
-                         int32_t *counts, void *stream) {
+tg_status tg_get_routing(tg_ctx *c, int n_tokens, int32_t *idx, float *w, int32_t *dst_rank, int32_t *dst_slot,
+                         int32_t *dst_pos, int32_t *counts, void *stream) {
   if (!c) return TG_ERR_INVALID;
   if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
+  if (n_tokens != c->last_T)
+    return fail(c, TG_ERR_INVALID, "tg_get_routing: n_tokens %d, the last call had %d", n_tokens, c->last_T);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(c->device));
   const size_t n = (size_t)c->last_T * c->k;
@@ -867,6 +997,8 @@ tg_status tg_kv_checkpoint(tg_ctx *c, const void *seg, size_t bytes, size_t offs
   CK(cudaStreamWaitEvent(c->kv_stream, c->kv_ev, 0));
   CK(cudaMemcpyAsync(c->kv_bucket + offset, seg, bytes, cudaMemcpyDeviceToHost, c->kv_stream));
   tg_ctx::KvRec *r = &c->kv_rec[c->kv_next % tg_ctx::kKvRecs];
+  if (c->kv_next >= tg_ctx::kKvRecs && c->kv_committed < r->seq)  // the record's commit is still pending
+    CK(cudaStreamSynchronize(c->kv_stream));
   ++c->kv_next;
   r->c = c;
   r->seq = seq;

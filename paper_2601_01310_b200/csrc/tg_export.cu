@@ -1,4 +1,4 @@
-// tg_kernels.cu — small auxiliary kernels of libtarragon (parity exports).
+// tg_export.cu — parity-export kernel of libtarragon (destination keys -> rank, bank slot).
 #include "tg_internal.h"
 
 namespace tg {

@@ -319,6 +319,8 @@ __device__ __forceinline__ void group_topk(const CallArgs &a, const RouteKeys &r
     }
   }
   __syncthreads();
+  if (a.logits)  // parity export: the fp32 logits the top-k below decides on
+    for (int i = threadIdx.x; i < n; i += bd) a.logits[(size_t)t0 * Er + i] = lsum[i + i / Er];
   if (grp == 0) TG_STAMP_ANY(31);
   // 256 threads = 32 tokens x 8; all lanes run every step (shuffles), writes are predicated
   const int r = threadIdx.x >> 3;
@@ -363,12 +365,20 @@ __device__ __forceinline__ void rank_chunk(const CallArgs &a, int chunk, uint8_t
 }
 
 // --------------------------------------------------------------------- P3
+// Count exchange.  Every rank writes its per-key totals into every live peer's
+// cnt_all[buf][src] and releases its count flag there; then it acquires every live
+// peer's flag.  A peer silent past cnt_timeout_ns is taken as failed for this run
+// (fail-stop; §5.2 "EWs tolerate AW failures"): its counts
+// are zero, it is recorded in the host-mapped fail mask and in sync[6] (the ranks
+// taking part in this run), so no row is dispatched to it, none of its rows is
+// awaited, and its combine flag is not awaited — no trap, the survivors complete
+// the run and tg_failover re-routes the pairs it held (NEXT-1).
 __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, int32_t *sm) {
   const int tid = threadIdx.x, nkeys = a.nkeys;
   int32_t *tot = sm;              // [nkeys] this rank's rows per key
   int32_t *gsum = sm + nkeys;     // [nkeys] rows per key over all sources
   int32_t *below = gsum + nkeys;  // [nkeys] rows per key from lower sources
-  const int par = a.xepoch & 1;
+  __shared__ uint32_t s_part;     // ranks taking part in this run
   const bool sys = a.world > 1;
   for (int K = tid; K < nkeys; K += blockDim.x) {
     int run = 0;
@@ -386,10 +396,10 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
     tot[K] = run;
     atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + K), (unsigned long long)run);
   }
+  if (tid == 0) s_part = a.alive | (1u << a.rank);
   __syncthreads();
-  if (a.world == 1 || a.replay) {
-    // no peers (or a failover replay, local by construction): the gathered counts are this
-    // rank's own, and only its own keys carry rows
+  if (a.world == 1) {
+    // no peers: the gathered counts are this rank's own, and only its own keys carry rows
     const int k0 = a.rank * a.S_max;
     for (int K = tid; K < nkeys; K += blockDim.x) {
       gsum[K] = tot[K];
@@ -412,29 +422,37 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
       a.sent_to[tid] = any > 0;
     }
     for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[k0 + s];
-    if (tid == 0) a.sync[5] = 0;  // no token dedup without peers
+    if (tid == 0) {
+      a.sync[5] = 0;  // no token dedup without peers
+      a.sync[6] = (int)(1u << a.rank);
+    }
     return;
   }
-  // all-gather: my totals -> cnt_all[par][rank][*] on every live peer, then release flags
+  // all-gather: my totals -> cnt_all[buf][rank][*] on every live peer, then release flags
   for (int q = 0; q < a.world; ++q) {
     if (!((a.alive >> q) & 1u)) continue;
-    int32_t *dst = reinterpret_cast<int32_t *>(a.sym[q] + a.L.cnt_all) + ((size_t)par * a.world + a.rank) * nkeys;
+    int32_t *dst = reinterpret_cast<int32_t *>(a.sym[q] + a.L.cnt_all) + ((size_t)a.cnt_buf * a.world + a.rank) * nkeys;
     for (int K = tid; K < nkeys; K += blockDim.x) dst[K] = tot[K];
   }
   __syncthreads();
   if (tid < a.world && ((a.alive >> tid) & 1u)) {
     fence_scope(sys);
-    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[tid] + a.L.flags) + FLAG_CNT * kMaxWorld + a.rank;
-    st_release(fl, a.xepoch, sys);
-    const uint32_t *mine = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + FLAG_CNT * kMaxWorld + tid;
-    wait_flag_ge_s(mine, a.xepoch, sys, a.err, 0x2001);
+    uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[tid] + a.L.flags) + a.fslot_cnt * kMaxWorld + a.rank;
+    st_release(fl, a.fepoch, sys);
+    const uint32_t *mine = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + a.fslot_cnt * kMaxWorld + tid;
+    if (tid != a.rank && !wait_flag_or_fail(mine, a.fepoch, sys, a.cnt_timeout_ns)) {
+      atomicOr(a.fail_mask, 1u << tid);  // silent peer: failed for this run (no trap)
+      atomicAnd(&s_part, ~(1u << tid));
+    }
   }
   __syncthreads();
-  const int32_t *A = reinterpret_cast<const int32_t *>(a.sym[a.rank] + a.L.cnt_all) + (size_t)par * a.world * nkeys;
+  const uint32_t part = s_part;
+  if (tid == 0) a.sync[6] = (int)part;
+  const int32_t *A = reinterpret_cast<const int32_t *>(a.sym[a.rank] + a.L.cnt_all) + (size_t)a.cnt_buf * a.world * nkeys;
   for (int K = tid; K < nkeys; K += blockDim.x) {
     int g = 0, bl = 0;
     for (int src = 0; src < a.world; ++src) {
-      const int c = ((a.alive >> src) & 1u) ? __ldcg(A + (size_t)src * nkeys + K) : 0;  // dead: no rows
+      const int c = src == a.rank ? tot[K] : ((part >> src) & 1u) ? __ldcg(A + (size_t)src * nkeys + K) : 0;
       if (src < a.rank) bl += c;
       g += c;
     }
@@ -444,13 +462,14 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
   }
   __syncthreads();
   // token dedup (NEXT-2) for calls that move many rows (prefill): every rank takes the same
-  // decision from the same all-gathered counts (global pairs x row bytes >= 16 MB)
+  // decision from the same all-gathered counts (global pairs x row bytes >= 16 MB); never in
+  // a failover replay
   if (tid < 32) {
     long long tot_pairs = 0;
     for (int K = tid; K < nkeys; K += 32) tot_pairs += gsum[K];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tot_pairs += __shfl_xor_sync(0xffffffffu, tot_pairs, o);
-    if (tid == 0) a.sync[5] = (tot_pairs * a.d * 2 >= (16ll << 20)) ? 1 : 0;
+    if (tid == 0) a.sync[5] = (!a.replay && tot_pairs * a.d * 2 >= (16ll << 20)) ? 1 : 0;
   }
   // dbase[K] = rows of lower slots on that rank (all sources) + rows of lower sources
   for (int K = tid; K < nkeys; K += blockDim.x) {
@@ -462,11 +481,12 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
   if (tid < a.world) {
     int to_me = 0, to_q = 0;
     for (int s = 0; s < a.S_max; ++s) {
-      to_me += ((a.alive >> tid) & 1u) ? __ldcg(A + (size_t)tid * nkeys + a.rank * a.S_max + s) : 0;
+      to_me += tid == a.rank ? tot[a.rank * a.S_max + s]
+                             : ((part >> tid) & 1u) ? __ldcg(A + (size_t)tid * nkeys + a.rank * a.S_max + s) : 0;
       to_q += tot[tid * a.S_max + s];
     }
     a.need_src[tid] = to_me > 0;
-    a.sent_to[tid] = to_q > 0;
+    a.sent_to[tid] = to_q > 0 && ((part >> tid) & 1u);
   }
   for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[a.rank * a.S_max + s];
 }
@@ -640,11 +660,15 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   TG_STAMP(3);
 }
 
-// In-call failover (NEXT-1, §5.1): replay of the last
-// call's pairs whose destination rank failed.  Every such pair takes the next live
-// candidate of its expert (rk = the resolution after masking the failed ranks),
-// which must be a shadow on this rank; the others keep their (good) outputs.  Then
-// P2 and a local P3 (no peer takes part) as in a normal call.
+// In-call failover (NEXT-1, §5.1 "the AW re-dispatches the affected
+// tokens ... to an alternate EW hosting the same expert (either a healthy primary
+// or a shadow)"): replay of the last call's pairs whose
+// destination rank failed.  Every such pair takes the next live candidate of its
+// expert (rk = the resolution after fail-stopping the failed ranks), on whichever
+// rank it lives; the other pairs keep their (good) outputs and get no key.  Then
+// P2 and the count exchange among the surviving ranks (replay flags and buffer),
+// so the replay rows are the whole work list of the destination EWs ("replayed
+// requests are prioritized").
 __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys &rk, uint8_t *fsm) {
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
   if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -658,10 +682,7 @@ __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys 
     int nk = -1;
     if (K >= 0 && ((a.failed >> (K / a.S_max)) & 1u)) {
       nk = rk.key[__ldcg(a.idx + p)];
-      if (nk < 0 || nk / a.S_max != a.rank) {  // next candidate on another rank: not in this call
-        atomicAdd(a.unrec, 1);
-        nk = -1;
-      }
+      if (nk < 0) atomicAdd(a.unrec, 1);  // no live candidate left (the host refuses such tables)
     }
     a.key[p] = nk;
   }
@@ -682,12 +703,17 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) 
   const int npairs = a.T * k;
   const int nsh = (a.Fsh > 0 && !a.replay) ? a.T : 0;  // a replay keeps the shared expert's output
   const bool dedup = __ldcg(a.sync + 5) != 0;
+  const uint32_t part = (uint32_t)__ldcg(a.sync + 6);  // ranks taking part in this run
   for (int p = w; p < npairs + nsh; p += nw) {
     if (p < npairs) {
       const int t = p / k;
       const int K = __ldcg(a.key + p);
       if (K < 0) continue;  // failover replay: pair not recomputed
       const int q = K / a.S_max;
+      if (!((part >> q) & 1u)) {  // destination failed in the count exchange: re-routed by tg_failover
+        if (lane == 0) a.dst_pos[p] = -1;
+        continue;
+      }
       const int pos =
           __ldcg(a.dbase + K) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K) + __ldcg(a.lrank + p);
       // token dedup (NEXT-2): a token goes once to each PEER rank; a later pair of the same
@@ -745,8 +771,9 @@ __device__ __forceinline__ void dispatch_done(const CallArgs &a) {
   fence_scope(sys);
   if (atomicAdd(&a.sync[3], 1) != (int)gridDim.x - 1) return;
   fence_scope(sys);
+  const uint32_t part = (uint32_t)__ldcg(a.sync + 6);
   for (int q = 0; q < a.world; ++q) {
-    if (!((a.alive >> q) & 1u)) continue;
+    if (!((part >> q) & 1u)) continue;
     uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[q] + a.L.flags) + a.fslot_data * kMaxWorld + a.rank;
     st_release(fl, a.fepoch, sys);
   }

@@ -56,9 +56,10 @@ struct GemmShared {
   int roff[kMaxPlan];      // reduction-group offsets
 };
 
-// silu(a) = a / (1 + e^-a) with the fast exp/divide (relative error ~1e-7, far
-// below the bf16 rounding of h that follows; the oracle computes it in fp64).
-__device__ __forceinline__ float silu_f(float a) { return __fdividef(a, 1.0f + __expf(-a)); }
+// silu(a) = a / (1 + e^-a) with IEEE expf (<= 2 ulp) and IEEE division (SURVEY 8(c) GPU
+// numerics rules): a few ulps of fp32, the part of the h bound of DESIGN.md R#24 that does
+// not come from the accumulation (the oracle computes it in fp64).
+__device__ __forceinline__ float silu_f(float a) { return __fdiv_rn(a, 1.0f + expf(-a)); }
 
 __device__ __forceinline__ int box_index(int nrows) { return ((nrows + 15) >> 4) - 1; }
 
@@ -629,22 +630,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   grid_barrier(gbar, a.epoch, 1, 0, err);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 16] = globaltimer_ns();
-  if (blockIdx.x == 0 && threadIdx.x < a.world && ((a.alive >> threadIdx.x) & 1u)) {
+  // combine flags: every rank taking part in this run waits for every other one (not only the
+  // EWs it sent rows to), so all survivors see a rank that fails mid-run in the same run and
+  // take part in the failover replay together; a peer silent past the failure timeout is
+  // recorded as failed (no trap), its pairs are re-routed by tg_failover (§5.1)
+  const uint32_t part = (uint32_t)__ldcg(a.sync + 6);
+  if (blockIdx.x == 0 && threadIdx.x < a.world && ((part >> threadIdx.x) & 1u)) {
     // every expert output this rank computed is in its source's combine buffer
     fence_scope(sys);
     uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[threadIdx.x] + a.L.flags) + a.fslot_comb * kMaxWorld + a.rank;
     st_release(fl, a.fepoch, sys);
   }
-  if (threadIdx.x < a.world && ((a.alive >> threadIdx.x) & 1u) && __ldcg(a.sent_to + threadIdx.x)) {
+  if (threadIdx.x < a.world && threadIdx.x != a.rank && ((part >> threadIdx.x) & 1u)) {
     const uint32_t *fl =
         reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + a.fslot_comb * kMaxWorld + threadIdx.x;
-    if (threadIdx.x == a.rank) {
-      wait_flag_ge_s(fl, a.fepoch, sys, err, 0x5001);
-    } else if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) {
-      // an EW that took rows from this rank failed mid-call: its pairs are recomputed by
-      // tg_failover on the shadows (in-call failover, §5.1)
-      atomicOr(a.fail_mask, 1u << threadIdx.x);
-    }
+    if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) atomicOr(a.fail_mask, 1u << threadIdx.x);
   }
   __syncthreads();
   const int nch = a.d >> 3;
@@ -706,10 +706,15 @@ cudaError_t layer_configure() {
 
 size_t layer_smem_bytes(const CallArgs &a) { return tg_max(gemm_smem_bytes(), front_smem(a)); }
 
-cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_sms, cudaStream_t s) {
+// n_ctas: one CTA per SM (cooperative launch: the grid barriers need every CTA resident), or
+// fewer when several virtual ranks share the GPU (tests: each rank's grid is a share of the
+// SMs, all resident at once; no cooperative attribute and no programmatic dependent launch,
+// whose early-resident CTAs could hold SMs another rank's grid is waiting for).
+cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_ctas, bool shared_gpu,
+                         cudaStream_t s) {
   if (layer_smem_bytes(a) > (size_t)kLayerSmemMax) return cudaErrorInvalidConfiguration;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_sms);
+  cfg.gridDim = dim3(n_ctas);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = layer_smem_bytes(a);
   cfg.stream = s;
@@ -719,7 +724,7 @@ cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = a.pdl ? 2 : 1;
+  cfg.numAttrs = shared_gpu ? 0 : (a.pdl ? 2 : 1);
   return cudaLaunchKernelEx(&cfg, k_layer, maps, a, rk);
 }
 

@@ -75,11 +75,13 @@ struct SymLayout {
   size_t meta;      // int2 [R_cap]               origin (src rank, t*k + j)
   size_t dup;       // int32 [R_cap]              token dedup: recv row to copy this row from (-1: sent)
   size_t ybuf;      // bf16 [T_max][k][d]         expert outputs returned to this AW
-  size_t cnt_all;   // int32 [2][world][nkeys]    all-gathered per-source counts
-  size_t flags;     // uint32 [5][kMaxWorld]      cnt / data / comb epoch flags, replay data / comb
+  size_t cnt_all;   // int32 [3][world][nkeys]    all-gathered per-source counts (calls by parity, replays)
+  size_t flags;     // uint32 [6][kMaxWorld]      cnt / data / comb epoch flags; replay data / comb / cnt
   size_t total;
 };
-constexpr int FLAG_CNT = 0, FLAG_DATA = 1, FLAG_COMB = 2, FLAG_RDATA = 3, FLAG_RCOMB = 4, kNumFlagKinds = 5;
+constexpr int FLAG_CNT = 0, FLAG_DATA = 1, FLAG_COMB = 2, FLAG_RDATA = 3, FLAG_RCOMB = 4, FLAG_RCNT = 5,
+              kNumFlagKinds = 6;
+constexpr int kCntBufReplay = 2;  // cnt_all buffer of failover replays (calls use 0 / 1 by parity)
 
 // Everything a call needs, by value (kernel parameter).
 struct CallArgs {
@@ -94,17 +96,18 @@ struct CallArgs {
   int g2dual;            // GEMM2 units cover two 128-row W2 tiles sharing one H tile (prefill-sized calls)
   uint32_t epoch;        // local kernel-run counter (grid barriers)
   uint32_t xepoch;       // cross-rank call counter (count flags, count parity): equal on every rank
-  uint32_t fepoch;       // value of this run's data / combine flags (xepoch, or epoch for a replay)
-  int fslot_data, fslot_comb;  // flag kinds of this run (FLAG_DATA/COMB, or FLAG_RDATA/RCOMB)
+  uint32_t fepoch;       // value of this run's count / data / combine flags (xepoch, or the replay counter)
+  int fslot_data, fslot_comb, fslot_cnt;  // flag kinds of this run (FLAG_DATA/COMB/CNT, or FLAG_R*)
+  int cnt_buf;           // cnt_all buffer of this run (xepoch & 1, or kCntBufReplay)
   // in-call failover (NEXT-1, §5.1)
   long long fail_timeout_ns;   // data / combine waits on peers: timeout -> peer failed (not a trap)
+  long long cnt_timeout_ns;    // count-exchange waits on peers (host threads may be late): timeout -> failed
   uint32_t *fail_mask;         // host-mapped: bit q = peer q failed during a call
   int *unrec;                  // host-mapped: replayed pairs whose next route is not on this rank
-  int replay;            // 1: recompute pairs routed to failed ranks (key_old) on this rank's shadows
+  int replay;            // 1: re-dispatch pairs routed to failed ranks (key_old) to their next live candidate
   uint32_t failed;       // replay: ranks whose pairs are recomputed
   const int32_t *key_old;  // replay: the failed call's destination keys
-  int inject_fail;
-  int dev_flag;          // development A/B switch (TG_DEVFLAG)       // fault injection (tests): stop after the dispatch, as a crash mid-call
+  int inject_fail;       // fault injection (tests): stop after the dispatch, as a crash mid-call
   // inputs / outputs
   const bf16 *x;
   bf16 *out;
@@ -128,7 +131,10 @@ struct CallArgs {
   int32_t *sent_to;      // [kMaxWorld] this rank sends rows to dest
   int32_t *slot_rows;    // [S_loc] M_s on this rank
   int64_t *stats;        // [nkeys]
-  int32_t *sync;         // [0..4] counters (scheduler, CTAs done, dispatch blocks, -, dedup copies), [5] dedup on; u64 grid barriers at [8], [10], [12]
+  int32_t *sync;         // [0..4] counters (scheduler, CTAs done, dispatch blocks, -, dedup copies), [5] dedup on,
+                         // [6] ranks taking part in this run (alive and heard from in the count exchange);
+                         // u64 grid barriers at [8], [10], [12]
+  float *logits;         // [T_max][E_r] router logits of the last call (parity export; nullptr = off)
   int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters
   int n_ctr_max;
   int32_t *n_units;      // [1] units of the last call (written by the GEMM, diagnostics)
@@ -146,10 +152,11 @@ struct CallArgs {
   SymLayout L;
 };
 
-// Kernel launchers (tg_kernels.cu / tg_gemm.cu).  Return cudaGetLastError().
+// Kernel launchers (tg_export.cu / tg_gemm.cu).  Return cudaGetLastError().
 // the whole layer call: one cooperative launch of k_layer (front P1-P3, then
 // dispatch || grouped GEMM, combine)
-cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_sms, cudaStream_t s);
+cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_ctas, bool shared_gpu,
+                         cudaStream_t s);
 cudaError_t launch_export_keys(const CallArgs &a, int n, int32_t *dst_rank, int32_t *dst_slot, cudaStream_t s);
 cudaError_t layer_configure();
 size_t gemm_smem_bytes();

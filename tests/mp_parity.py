@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import workloads as wl  # noqa: E402
-from parity_util import compare, oracle_layer  # noqa: E402
+from parity_util import check, collect  # noqa: E402
 
 
 def main():
@@ -56,6 +56,7 @@ def main():
     pl = wl.make_placement(sh.E, W, world)
     layer = tg.MoELayer(sh, pl, L, max_tokens_per_rank=Tr, rank=rank, world=world, device=local,
                         group=dist.group.WORLD)
+    layer.export_stages(True)
     xr = x[rank * Tr:(rank + 1) * Tr].contiguous().to(dev)
     rep = {"rank": rank, "world": world, "W": W, "config": a.config, "T": T}
     ok = True
@@ -72,29 +73,22 @@ def main():
         return torch.cat(outs).cpu()
 
     out = run()
-    rt = layer.routing(Tr)
     out_all = gather(out)
-    # routing tensors of all ranks (rank order = global token order)
-    rt_all = {}
-    for kname in ("idx", "w", "dst_rank", "dst_slot", "dst_pos"):
-        t = rt[kname].contiguous()
-        parts = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(parts, t)
-        rt_all[kname] = torch.cat(parts)
-    rt_all["counts"] = rt["counts"]
+    # every rank's routing and stage exports -> rank 0, which checks them all against the oracle
+    views = [None] * world
+    dist.all_gather_object(views, collect(layer, out, t0=rank * Tr))
     if rank == 0:
         if a.sample:
             rng = np.random.default_rng(seed)
             tok = np.sort(rng.choice(T, size=min(a.sample, T), replace=False)).astype(np.int32)
         else:
             tok = None
-        ref = oracle_layer(L, x, pl, [0] * W, G=world, tokens=tok, n_threads=min(32, os.cpu_count() or 1))
         try:
-            o_u16 = wl.as_u16(out_all)
-            rep["parity"] = compare(ref, o_u16 if tok is None else o_u16[tok], rt_all, tokens=tok)
+            rep["parity"] = check(views, L, x, pl, [0] * W, tokens=tok, n_threads=min(32, os.cpu_count() or 1))
         except AssertionError as e:
             ok = False
             msgs.append(f"parity: {e}")
+    del views
     # determinism
     out2 = run()
     if not torch.equal(out.view(torch.int16), out2.view(torch.int16)):
@@ -230,8 +224,8 @@ def inflight_fail_checks(tg, layer, rank, world, out, run, xr, msgs, rep):
     """NEXT-1 (§5.1): the last rank crashes in the middle of a call (after its count
     exchange and dispatch, before its expert outputs).  Survivors detect it within that call
     (failure timeout on its combine flag), and tg_failover recomputes the pairs they had sent it
-    on the shadows: the repaired output of THAT call must be bitwise the unfailed output.  With
-    2 ranks every shadow of the dead rank's experts is on the survivor (spread placement)."""
+    to the next live candidate of each expert on whichever surviving rank hosts it: the repaired
+    output of THAT call must be bitwise the unfailed output, at any G (cross-rank replay)."""
     import time
     ok = True
     dead = world - 1
@@ -251,13 +245,12 @@ def inflight_fail_checks(tg, layer, rank, world, out, run, xr, msgs, rep):
         if failed != (1 << dead):
             ok = False
             msgs.append(f"rank {rank}: failed mask {failed:#x}, expected {1 << dead:#x}")
-        if world == 2:
-            if rc != tg.TG_OK:
-                ok = False
-                msgs.append(f"rank {rank}: failover rc {rc}")
-            if not torch.equal(out.view(torch.int16), o.view(torch.int16)):
-                ok = False
-                msgs.append(f"rank {rank}: repaired output differs ({int((out != o).sum())} elements)")
+        if rc != tg.TG_OK:
+            ok = False
+            msgs.append(f"rank {rank}: failover rc {rc}")
+        if not torch.equal(out.view(torch.int16), o.view(torch.int16)):
+            ok = False
+            msgs.append(f"rank {rank}: repaired output differs ({int((out != o).sum())} elements)")
         # the next calls run without the dead rank (fail-stop, NEXT-3a)
         for i in range(3):
             o2 = run()

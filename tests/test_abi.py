@@ -158,3 +158,35 @@ def test_failover_and_host_path_host_only():
     assert tg._lib.tg_host_sync(ctx, None) == tg.TG_ERR_UNSUPPORTED
     assert tg.tg_inject_failure(ctx) == tg.TG_OK  # a flag for the next call (none can run here)
     tg.tg_finalize(ctx)
+
+
+def test_load_experts_guards_active_table_slots():
+    """a slot the active route table names for expert e cannot be overwritten with
+    another expert (it would silently serve e's tokens with wrong weights); same expert is fine."""
+    tg, ctx, pl = _host_ctx()
+    assert tg.tg_set_route_table(ctx, 1, pl.cand) == tg.TG_OK
+    e0 = pl.hosted[0][0]
+    tg.tg_load_experts(ctx, 0, 0, e0, None, None, None)  # reload of the same expert: allowed
+    with pytest.raises(tg.TarragonError) as ei:
+        tg.tg_load_experts(ctx, 0, 0, (e0 + 1) % 8, None, None, None)
+    assert ei.value.status == tg.TG_ERR_INVALID and "route table" in str(ei.value)
+    tg.tg_finalize(ctx)
+
+
+def test_virtual_rank_and_stage_calls_host_only():
+    """Host-only ctxs refuse the device-side bootstrap / export entry points."""
+    tg, ctx, pl = _host_ctx()
+    for fn, args in ((tg.tg_set_launch_ctas, (4,)), (tg.tg_set_stage_export, (1,)),
+                     (tg.tg_connect_local, ([ctx],))):
+        with pytest.raises(tg.TarragonError) as ei:
+            fn(ctx, *args)
+        assert ei.value.status == tg.TG_ERR_UNSUPPORTED
+    with pytest.raises(tg.TarragonError):
+        tg.tg_get_stage(ctx, tg.TG_STAGE_Y)
+    tg.tg_finalize(ctx)
+
+
+def test_peer_handle_carries_layout_signature():
+    """The peer handle is the IPC handle plus the layout signature checked at connect time."""
+    tg = _tg()
+    assert tg.tg_peer_handle_size() >= 64 + 64

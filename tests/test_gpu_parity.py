@@ -1,5 +1,7 @@
 """GPU (sm_100a) parity of the C-ABI path against the CPU oracle (criteria P1-P8,
-SURVEY.md 8(c)); every call goes through libtarragon.so via the binding."""
+SURVEY.md 8(c)); every call goes through libtarragon.so via the binding, and
+every bf16 storage point is checked against the oracle's exact value of that
+stage (tests/parity_util.py, R#21 / R#24)."""
 import os
 
 import numpy as np
@@ -7,7 +9,7 @@ import pytest
 import torch
 
 import workloads as wl
-from parity_util import compare, oracle_layer
+from parity_util import check, collect, oracle_layer, single
 
 pytestmark = pytest.mark.gpu
 
@@ -21,7 +23,7 @@ def _tg():
 
 def _setup(cfg, W, seed, T=None, skew=0.0, integer=False, shadows=True, T_max=None):
     tg = _tg()
-    sh = wl.CONFIGS[cfg]
+    sh = wl.CONFIGS[cfg] if isinstance(cfg, str) else cfg
     T = sh.T if T is None else T
     u = None
     if skew:
@@ -31,6 +33,7 @@ def _setup(cfg, W, seed, T=None, skew=0.0, integer=False, shadows=True, T_max=No
     x = wl.integer_tokens(sh, seed, T) if integer else wl.make_tokens(sh, seed, T, skew_mu=skew, u=u)
     pl = wl.make_placement(sh.E, W, 1, shadows=shadows)
     layer = tg.MoELayer(sh, pl, L, max_tokens_per_rank=T_max or max(T, 1))
+    layer.export_stages(True)
     return tg, sh, L, x, pl, layer
 
 
@@ -43,7 +46,6 @@ def _run(layer, x):
 
 def test_library_is_native_and_loaded():
     tg = _tg()
-    import ctypes  # noqa: F401
     assert os.path.exists(tg.LIB_PATH)
     with open("/proc/self/maps") as f:
         assert "libtarragon.so" in f.read()
@@ -54,9 +56,7 @@ def test_tiny_parity_mask_poison_flip(skew):
     """configs[0]: tiny layer, 2 logical EWs with shadows on one B200; EW1 masked mid-run."""
     tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1000, skew=skew)
     out0 = _run(layer, x)
-    rt = layer.routing(x.shape[0])
-    ref = oracle_layer(L, x, pl, [0, 0], G=1)
-    rep = compare(ref, wl.as_u16(out0), rt)
+    rep = single(layer, out0, L, x, pl, [0, 0])
     print("tiny", skew, rep)
     # P6 determinism
     out0b = _run(layer, x)
@@ -81,9 +81,7 @@ def test_tiny_parity_mask_poison_flip(skew):
     st1 = layer.stats() - st0
     for sl in range(pl.slots_per_ew):
         assert st1[0, base[1] + sl] == 0, "masked EW received rows"
-    rt1 = layer.routing(x.shape[0])
-    ref1 = oracle_layer(L, x, pl, [0, 1], G=1)
-    compare(ref1, wl.as_u16(out1), rt1)
+    single(layer, out1, L, x, pl, [0, 1])
 
 
 def test_route_flip_bit_identity():
@@ -95,26 +93,26 @@ def test_route_flip_bit_identity():
         assert layer.set_route_table(cand) == tg.TG_OK
         o = _run(layer, x)
         assert torch.equal(outA.view(torch.int16), o.view(torch.int16)), f"flip {i} changed output"
-        rt = layer.routing(x.shape[0])
         pl2 = wl.Placement(pl.n_ews, pl.ew_rank, pl.slots_per_ew, pl.hosted, cand)
-        ref = oracle_layer(L, x, pl2, [0, 0], G=1)
-        compare(ref, wl.as_u16(o), rt)
+        single(layer, o, L, x, pl2, [0, 0])
     # stale versions are ignored
     assert tg.tg_set_route_table(layer.ctx, layer.version, pl.cand) == tg.TG_ERR_STALE_VERSION
+    # a slot the active table names for another expert cannot be overwritten
+    e0 = pl.hosted[0][0]
+    other = (e0 + 1) % sh.E
+    with pytest.raises(tg.TarragonError):
+        tg.tg_load_experts(layer.ctx, 0, 0, other, L.w1[other], L.w3[other], L.w2[other])
 
 
 def test_integer_ties_bit_exact():
     """Integer router inputs: logits exact in any order, so lowest-id tie breaks must match exactly."""
     tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1002, integer=True)
     out = _run(layer, x)
-    rt = layer.routing(x.shape[0])
     ref = oracle_layer(L, x, pl, [0, 0], G=1)
-    assert np.array_equal(rt["idx"].cpu().numpy(), ref["idx"])
     assert (ref["gap"] == 0).sum() > 10, "test needs exact ties"
-    for kk in ("dst_rank", "dst_slot", "dst_pos"):
-        assert np.array_equal(rt[kk].cpu().numpy(), ref[kk])
-    ref["gap"][:] = 1.0  # no near-tie exemption
-    compare(ref, wl.as_u16(out), rt)
+    ref["gap"][:] = 1.0  # no near-tie exemption: idx and permutation bit-exact for every token
+    rep = single(layer, out, L, x, pl, [0, 0], ref=ref)
+    assert rep["max_dlogit"] == 0.0
 
 
 @pytest.mark.parametrize("T", [1, 37, 300, 1000])
@@ -122,9 +120,27 @@ def test_ragged_and_multi_tile(T):
     """Ragged token counts; T = 1000 gives ~250 rows per expert -> 2 token tiles (128 + ragged)."""
     tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1003 + T, T=T)
     out = _run(layer, x)
-    rt = layer.routing(T)
-    ref = oracle_layer(L, x, pl, [0, 0], G=1)
-    compare(ref, wl.as_u16(out), rt)
+    single(layer, out, L, x, pl, [0, 0])
+
+
+@pytest.mark.parametrize("shape", [
+    wl.Shape("k1_E1", d=64, E=1, k=1, F=128, T=200),     # dense SwiGLU FFN through the MoE path
+    wl.Shape("k1_E8", d=128, E=8, k=1, F=192, T=300),    # w = 1 exactly, out = y
+    wl.Shape("kE_8", d=64, E=8, k=8, F=128, T=256),      # k = E: dense softmax mixture, gap = +inf
+], ids=lambda s: s.name)
+def test_degenerate_k_and_E(shape):
+    """The method's degenerate cases (SURVEY 8(c) special cases) through the GPU path."""
+    tg, sh, L, x, pl, layer = _setup(shape, 2, seed=1020)
+    out = _run(layer, x)
+    rep = single(layer, out, L, x, pl, [0, 0])
+    rt = layer.routing(x.shape[0])
+    if sh.k == 1:
+        assert torch.all(rt["w"] == 1.0)
+    if sh.k == sh.E:
+        assert rep["near_ties"] == 0
+        assert torch.equal(rt["idx"].cpu(), torch.arange(sh.E, dtype=torch.int32).expand(x.shape[0], sh.E))
+    layer.mask_worker(1, 1)
+    assert torch.equal(out.view(torch.int16), _run(layer, x).view(torch.int16))
 
 
 @pytest.mark.parametrize("mode", ["TG_WIDE", "TG_G2DUAL"])
@@ -136,7 +152,7 @@ def test_tile_modes_parity(cfg, T, mode, monkeypatch):
     if cfg == "tiny":
         tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1006, T=T)
         out = _run(layer, x)
-        compare(oracle_layer(L, x, pl, [0, 0], G=1), wl.as_u16(out), layer.routing(T))
+        single(layer, out, L, x, pl, [0, 0])
         layer.mask_worker(1, 1)
         assert torch.equal(out.view(torch.int16), _run(layer, x).view(torch.int16))
     else:
@@ -165,9 +181,11 @@ def test_empty_call_and_errors():
     tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1004, T=16, T_max=64)
     empty = torch.empty(0, sh.d, dtype=torch.bfloat16, device="cuda")
     assert tg.tg_moe_layer(layer.ctx, empty, torch.empty_like(empty)) == tg.TG_OK
+    torch.cuda.synchronize()
+    with pytest.raises(tg.TarragonError):  # routing export is sized by the last call's tokens
+        layer.routing(16)
     out = _run(layer, x)
-    ref = oracle_layer(L, x, pl, [0, 0], G=1)
-    compare(ref, wl.as_u16(out), layer.routing(16))
+    single(layer, out, L, x, pl, [0, 0])
     # too many tokens
     big = torch.zeros(65, sh.d, dtype=torch.bfloat16, device="cuda")
     assert tg.tg_moe_layer(layer.ctx, big, torch.empty_like(big)) == tg.TG_ERR_INVALID
@@ -203,18 +221,19 @@ def test_host_entry_point_e2e():
         assert torch.equal(o.view(torch.int16), ref.view(torch.int16))
 
 
-def _big(cfg, seed, n_sample, W=2, T=None):
-    tg, sh, L, x, pl, layer = _setup(cfg, W, seed=seed, T=T)
+def _big(cfg, seed, n_sample, W=2, T=None, skew=0.0):
+    tg, sh, L, x, pl, layer = _setup(cfg, W, seed=seed, T=T, skew=skew)
     out = _run(layer, x)
-    rt = layer.routing(x.shape[0])
     Tn = x.shape[0]
-    rng = np.random.default_rng(seed)
-    tok = np.sort(rng.choice(Tn, size=min(n_sample, Tn), replace=False)).astype(np.int32)
-    tok[0] = 0
-    tok[-1] = Tn - 1
-    ref = oracle_layer(L, x, pl, [0] * W, G=1, tokens=tok, n_threads=NT)
-    rep = compare(ref, wl.as_u16(out)[tok], rt, tokens=tok)
-    print(cfg, rep)
+    if n_sample is None or n_sample >= Tn:
+        tok = None
+    else:
+        rng = np.random.default_rng(seed)
+        tok = np.sort(rng.choice(Tn, size=n_sample, replace=False)).astype(np.int32)
+        tok[0] = 0
+        tok[-1] = Tn - 1
+    rep = single(layer, out, L, x, pl, [0] * W, tokens=tok, n_threads=NT)
+    print(cfg, "skew" if skew else "", rep)
     # mask EW1: bit-identical at full size
     layer.mask_worker(1, 1)
     out1 = _run(layer, x)
@@ -223,9 +242,10 @@ def _big(cfg, seed, n_sample, W=2, T=None):
     return rep
 
 
-def test_mixtral_decode_parity():
-    """configs[1]: Mixtral-shaped layer, T = 256 decode batch; routing for all tokens, FFN on a sample."""
-    _big("mixtral_decode", 2001, n_sample=24)
+def test_mixtral_decode_parity_full_T():
+    """configs[1]: Mixtral-shaped layer, T = 256 decode batch; routing AND the FFN of every token
+    (full-T FFN parity on Mixtral decode)."""
+    _big("mixtral_decode", 2001, n_sample=None)
 
 
 def test_ds_v2_lite_shared_parity():
@@ -236,6 +256,12 @@ def test_ds_v2_lite_shared_parity():
 def test_qwen_prefill_parity():
     """configs[4] shape: 60 experts top-4, prefill T = 8192 (multi-tile slots)."""
     _big("qwen_prefill", 2003, n_sample=48, W=4)
+
+
+@pytest.mark.parametrize("cfg,W", [("ds_v2_lite_decode", 8), ("qwen_prefill", 4)])
+def test_skewed_routing_parity(cfg, W):
+    """App. B imbalance: skewed routing (top expert ~3x the mean load) at full size."""
+    _big(cfg, 2006, n_sample=32, W=W, skew=0.6)
 
 
 @pytest.mark.parametrize("cfg,W", [("ds_v2_lite_decode_g1", 8), ("qwen_prefill_sg", 4)])
