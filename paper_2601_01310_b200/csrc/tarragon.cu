@@ -296,7 +296,10 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
   size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
   size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(64);
-  size_t o_ctr = carve((size_t)c->args.n_ctr_max * 4);
+  const int n_grp_max = nt_max + nt_sh + 16;
+  c->args.n_ctr_all = c->args.n_ctr_max + n_grp_max + (int)Tm;
+  size_t o_ctr = carve((size_t)c->args.n_ctr_all * 4);
+  size_t o_srow = carve((size_t)c->R_cap * 4 + 4);
   size_t o_nu = carve(16);
   size_t o_H = carve((size_t)c->R_cap * F * 2);
   size_t o_Hs = carve(Fsh > 0 ? Tm * Fsh * 2 : 0);
@@ -327,6 +330,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
   a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
   a.sync = (int32_t *)(sb + o_sync); a.ctr = (int32_t *)(sb + o_ctr);
+  a.rdy = a.ctr + a.n_ctr_max; a.tokctr = a.rdy + n_grp_max; a.srcrow = (int32_t *)(sb + o_srow);
   a.n_units = (int32_t *)(sb + o_nu);
   a.H = (bf16 *)(sb + o_H); a.Hs = Fsh > 0 ? (bf16 *)(sb + o_Hs) : nullptr;
   a.ws = c->nsplit > 1 ? (float *)(sb + o_ws) : nullptr; a.ysh = Fsh > 0 ? (bf16 *)(sb + o_ysh) : nullptr;

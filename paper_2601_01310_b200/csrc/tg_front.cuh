@@ -60,6 +60,14 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t &r0, uint32_t &r1, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+
 __host__ __device__ __forceinline__ int router_kpart(int d, int E) {
   int kp = E <= 96 ? 512 : (E <= 192 ? 256 : 128);
   while (kp > 64 && d % kp) kp >>= 1;  // d % 64 == 0, so 64 always divides d
@@ -69,114 +77,170 @@ __host__ __device__ __forceinline__ int router_nkp(int d, int E) { return (d + r
 __host__ __device__ __forceinline__ int router_epad(int E) { return (E + 63) / 64 * 64; }
 
 
-struct RouterSmem {
-  uint32_t *wg;   // [Epad][KP/2 + 4] words
-  uint32_t *xt;   // [32][KP/2 + 4] words
-  float *part;    // [8][32][64]
-  int ldw;        // row stride in words
-};
-
-// Batched copy of rows of 16-B chunks into padded smem rows: 16 loads in flight per
-// thread before the stores (these loops are latency-bound, not bandwidth-bound).
-template <typename RowPtr, typename DstRow>
-__device__ __forceinline__ void stage_rows(int nrows, int cpr, RowPtr row, DstRow drow) {
-  const int total = nrows * cpr;
-  const int lc = __ffs(cpr) - 1;  // cpr = KP / 8 is a power of two
-#pragma unroll 1
-  for (int i0 = threadIdx.x; i0 < total; i0 += 16 * blockDim.x) {
-    uint4 v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u * blockDim.x;
-      const uint4 *p = (i < total) ? row(i >> lc) : nullptr;
-      v[u] = p ? __ldg(p + (i & (cpr - 1))) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i < total) *reinterpret_cast<uint4 *>(drow(i >> lc) + (i & (cpr - 1)) * 4) = v[u];
-    }
-  }
+// Router work decomposition, a function of E only (so every call computes a logit with
+// the same arithmetic): the n8 expert tiles of an item are spread over the 8 warps and, when
+// there are fewer than 8 tiles, the K part is cut into nsub sub-slices (powers of two) whose
+// fp64 partials are summed in K order through shared memory.
+__host__ __device__ __forceinline__ int router_ntiles(int E) { return (E + 7) / 8; }
+__host__ __device__ __forceinline__ int router_nsub(int d, int E) {
+  const int nt = min(router_ntiles(E), 8), steps = router_kpart(d, E) / 16;
+  int ns = 1;
+  while (ns * 2 * nt <= 8 && ns * 2 <= steps) ns *= 2;
+  return ns;
 }
 
-__device__ void router_item(const CallArgs &a, const RouterSmem &R, int grp, int kp, bool with_wg) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = a.d, E = a.E_r, T = a.T;  // router rows: experts (+ shared-gate row)
-  const int g = lane >> 2, c = lane & 3;
-  const int KP = router_kpart(d, E), nkp = router_nkp(d, E), Epad = router_epad(E);
+constexpr int kXBufMax = 4;                 // router x tiles in flight per block
+constexpr int kFrontBudget = 224 * 1024;    // dynamic smem of the front phases
+
+__host__ __device__ __forceinline__ size_t router_wg_bytes(int d, int E) {
+  return (size_t)router_epad(E) * (router_kpart(d, E) / 2 + 4) * 4;
+}
+__host__ __device__ __forceinline__ size_t router_xtile_bytes(int d, int E) {
+  return (size_t)kRouterRows * (router_kpart(d, E) / 2 + 4) * 4;
+}
+__host__ __device__ __forceinline__ size_t router_red_bytes() { return (size_t)8 * kRouterRows * 8 * sizeof(double); }
+// Scratch after the x ring: the router's fp64 sub-slice partials, then (aliased, used after an
+// item's compute) the group top-k logits, the chunk rank bitmaps and the exchange arrays.
+__host__ __device__ __forceinline__ size_t front_scratch_bytes(int E_r, int nkeys) {
+  const size_t topk = sizeof(float) * ((size_t)kRouterRows * (E_r + 1) + kRouterRows * kMaxK);
+  size_t m = router_red_bytes();
+  if (topk > m) m = topk;
+  if ((size_t)32 * nkeys > m) m = (size_t)32 * nkeys;
+  if ((size_t)12 * nkeys + 64 > m) m = (size_t)12 * nkeys + 64;
+  return (m + 15) / 16 * 16;
+}
+__host__ __device__ __forceinline__ int router_nbuf(int d, int E, int nkeys) {
+  const long long room =
+      (long long)kFrontBudget - (long long)router_wg_bytes(d, E) - (long long)front_scratch_bytes(E, nkeys);
+  const long long n = room / (long long)router_xtile_bytes(d, E);
+  return n < 1 ? 1 : (n > kXBufMax ? kXBufMax : (int)n);
+}
+
+struct RouterSmem {
+  uint32_t *wg;   // [Epad][ldw] words: this block's K part of Wg, staged once
+  uint32_t *xt;   // [nbuf][32][ldw] words: x tiles in flight (cp.async ring)
+  double *red;    // [8][32][8] fp64 partials of the K sub-slices
+  uint8_t *tail;  // group top-k, rank bitmaps, exchange arrays (alias red, not the ring)
+  int ldw, nbuf;
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Issue the cp.async loads of item (grp, kp) into ring buffer `buf` (x tile; and the Wg slice on
+// the block's first item), then commit one group.  Rows past T are clamped (never used).
+__device__ __forceinline__ void router_issue(const CallArgs &a, const RouterSmem &R, int grp, int kp, int buf,
+                                             bool with_wg) {
+  const int d = a.d, E = a.E_r, T = a.T;
+  const int KP = router_kpart(d, E), cpr = KP / 8, lc = __ffs(cpr) - 1;
+  if (with_wg) {
+    const int nw = E * cpr;
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+      const int r = i >> lc, c = i & (cpr - 1);
+      cp_async16(R.wg + r * R.ldw + c * 4, a.wg + (size_t)r * d + kp * KP + c * 8);
+    }
+  }
   const int t0 = grp * kRouterRows;
-  const int cpr = KP / 8;
-  if (grp == 0 && kp == 0) TG_STAMP(10);
-  // x tile [32][KP] -> smem (rows past T clamped; their results are never used); on the
-  // block's first item the Wg slice [E8][KP] joins the same load batch (one latency)
-  const int E8 = with_wg ? (E + 7) / 8 * 8 : 0;  // Wg rows of the n8 tiles actually used
-  stage_rows(
-      E8 + kRouterRows, cpr,
-      [&](int r) -> const uint4 * {
-        if (r < E8) return r < E ? reinterpret_cast<const uint4 *>(a.wg + (size_t)r * d + kp * KP) : nullptr;
-        return reinterpret_cast<const uint4 *>(a.x + (size_t)min(t0 + r - E8, T - 1) * d + kp * KP);
-      },
-      [&](int r) -> uint32_t * { return (r < E8 ? R.wg + r * R.ldw : R.xt + (r - E8) * R.ldw); });
-  __syncthreads();
-  if (grp == 0 && kp == 0) TG_STAMP(11);
-  const int ksw = max(16, KP / 8);   // K elements of this warp (multiple of 16)
-  const int nsteps = (warp * ksw < KP) ? ksw / 16 : 0;
-  const int wk0 = warp * ksw / 2;    // first word column
+  uint32_t *xb = R.xt + (size_t)buf * kRouterRows * R.ldw;
+  const int nx = kRouterRows * cpr;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    const int r = i >> lc, c = i & (cpr - 1);
+    cp_async16(xb + r * R.ldw + c * 4, a.x + (size_t)min(t0 + r, T - 1) * d + kp * KP + c * 8);
+  }
+  cp_async_commit();
+}
+
+// P1 item: partial logits of 32 tokens over K part kp from ring buffer `buf` (landed, block
+// synced).  mma.sync m16n8k16 (bf16 products exact in fp32); a warp accumulates its K range in
+// sets of 8 k16 steps, each in its own fp32 registers, the sets summed in fp64 in K order
+// (shorter fp32 chains: ~1 ulp of logit instead of several), sub-slices likewise through smem;
+// the part's sum is stored rounded to fp32.  Order fixed by (d, E): deterministic, row-invariant.
+__device__ void router_compute(const CallArgs &a, const RouterSmem &R, int grp, int kp, int buf) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = a.d, E = a.E_r;
+  const int g = lane >> 2, c = lane & 3;
+  const int KP = router_kpart(d, E), nkp = router_nkp(d, E);
+  const int ntl = router_ntiles(E), nsub = router_nsub(d, E), nte = min(ntl, 8);
+  const int steps = KP / 16 / nsub;               // k16 steps of one sub-slice
+  const uint32_t *xb = R.xt + (size_t)buf * kRouterRows * R.ldw;
   float *dst = a.logit_part + ((size_t)grp * nkp + kp) * kRouterRows * E;
-  for (int e0 = 0; e0 < Epad; e0 += 64) {
-    const int ntr = min(8, (E - e0 + 7) / 8);  // n8 tiles holding real experts
-    float acc[2][8][4];
+  for (int eb = 0; eb < ntl; eb += 8) {          // expert blocks of 8 n8 tiles (E > 64)
+    const int tile = eb + warp % nte, sub = warp / nte;
+    const bool act = (warp < nte * nsub) && (tile < ntl);
+    double v[2][4];
+    if (act) {
+      // fragments by ldmatrix: A (x, row-major 16 x 16 per m) as x4, B (Wg rows = experts, k
+      // contiguous = the .col operand) as x2; lane L addresses row L & 15 (A) / L & 7 (B)
+      const uint32_t xa = smem_u32(xb + (lane & 15) * R.ldw) + (lane >> 4) * 16;
+      const uint32_t wa = smem_u32(R.wg + (tile * 8 + (lane & 7)) * R.ldw) + ((lane >> 3) & 1) * 16;
+      const uint32_t mstr = 16 * R.ldw * 4;  // bytes between the two m16 row blocks
+      const int k0 = sub * steps;            // first k16 step of this warp's sub-slice
+      const int nsets = (steps + 7) / 8;
+      float acc[4][2][4];
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int n = 0; n < 8; ++n)
+        for (int m = 0; m < 2; ++m)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[m][n][i] = 0.f;
-    for (int s = 0; s < nsteps; ++s) {
-      const int wc = wk0 + 8 * s + c;  // word column of k = 16 s + 2 c
-      uint32_t af[2][4];
+          for (int i = 0; i < 4; ++i) acc[q][m][i] = 0.f;
+      // the sets' steps interleaved: 8 independent accumulator chains per warp (the set a
+      // step belongs to, not the issue order, decides where it is summed)
+      for (int st = 0; st < 8; ++st) {
 #pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const uint32_t *x0 = R.xt + (16 * m + g) * R.ldw, *x1 = x0 + 8 * R.ldw;
-        af[m][0] = x0[wc];
-        af[m][1] = x1[wc];
-        af[m][2] = x0[wc + 4];
-        af[m][3] = x1[wc + 4];
-      }
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        if (n < ntr) {
-          const uint32_t *wr = R.wg + (e0 + 8 * n + g) * R.ldw;
-          const uint32_t b0 = wr[wc], b1 = wr[wc + 4];
-          mma_bf16_16816(acc[0][n], af[0], b0, b1);
-          mma_bf16_16816(acc[1][n], af[1], b0, b1);
+        for (int q = 0; q < 4; ++q) {
+          const int kstep = q * 8 + st;
+          if (q < nsets && kstep < steps) {
+            const uint32_t off = (uint32_t)(k0 + kstep) * 32;  // 16 bf16 = 32 B per k16 step
+            uint32_t a0[4], a1[4], b0, b1;
+            ldsm_x4(a0, xa + off);
+            ldsm_x4(a1, xa + mstr + off);
+            ldsm_x2(b0, b1, wa + off);
+            mma_bf16_16816(acc[q][0], a0, b0, b1);
+            mma_bf16_16816(acc[q][1], a1, b0, b1);
+          }
         }
       }
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double sum = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < nsets) sum += (double)acc[q][m][i];
+          v[m][i] = sum;
+        }
     }
+    // lane holds rows 16m + g (+8 for i >= 2), experts 8 tile + 2c (+1 for odd i)
+    if (nsub == 1) {
+      if (act)
 #pragma unroll
-    for (int m = 0; m < 2; ++m)
+        for (int m = 0; m < 2; ++m)
 #pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        if (n >= ntr) continue;
-        float *p = R.part + (warp * kRouterRows + 16 * m) * 64 + 8 * n + 2 * c;
-        p[g * 64] = acc[m][n][0];
-        p[g * 64 + 1] = acc[m][n][1];
-        p[(g + 8) * 64] = acc[m][n][2];
-        p[(g + 8) * 64 + 1] = acc[m][n][3];
+          for (int i = 0; i < 4; ++i) {
+            const int row = 16 * m + g + 8 * (i >> 1), e = tile * 8 + 2 * c + (i & 1);
+            if (e < E) dst[row * E + e] = (float)v[m][i];
+          }
+    } else {
+      if (act)
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            R.red[(warp * kRouterRows + 16 * m + g + 8 * (i >> 1)) * 8 + 2 * c + (i & 1)] = v[m][i];
+      __syncthreads();
+      for (int i = threadIdx.x; i < kRouterRows * nte * 8; i += blockDim.x) {
+        const int row = i / (nte * 8), col = i % (nte * 8), tl = col / 8, e = (eb + tl) * 8 + (col & 7);
+        double sum = 0.0;
+        for (int sb = 0; sb < nsub; ++sb) sum += R.red[((sb * nte + tl) * kRouterRows + row) * 8 + (col & 7)];
+        if (e < E) dst[row * E + e] = (float)sum;
       }
-    __syncthreads();
-    const int ew = min(64, E - e0);
-    for (int i = threadIdx.x; i < kRouterRows * ew; i += blockDim.x) {
-      const int r = i / ew, ee = i % ew, e = e0 + ee;
-      {
-        const int pi = r * 64 + ee;
-        float sum = R.part[pi];
-#pragma unroll
-        for (int ww = 1; ww < 8; ++ww) sum += R.part[ww * kRouterRows * 64 + pi];
-        dst[r * E + e] = sum;
-      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -296,7 +360,7 @@ __device__ __forceinline__ void group_topk(const CallArgs &a, const RouteKeys &r
   const int bd = blockDim.x;
 #pragma unroll 1
   for (int i0 = threadIdx.x; i0 < n; i0 += 4 * bd) {
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    double s[4] = {0.0, 0.0, 0.0, 0.0};  // parts summed in fp64 in part order, rounded once
 #pragma unroll 1
     for (int q0 = 0; q0 < nkp; q0 += 4) {
       float p[4][4];
@@ -310,12 +374,12 @@ __device__ __forceinline__ void group_topk(const CallArgs &a, const RouteKeys &r
       for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (q0 + q < nkp) s[u] = (q0 + q == 0) ? p[u][q] : s[u] + p[u][q];
+          if (q0 + q < nkp) s[u] += (double)p[u][q];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int i = i0 + u * bd;
-      if (i < n) lsum[i + i / Er] = s[u];  // row i / Er, padded stride Er + 1
+      if (i < n) lsum[i + i / Er] = (float)s[u];  // row i / Er, padded stride Er + 1
     }
   }
   __syncthreads();
@@ -382,12 +446,12 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
   const bool sys = a.world > 1;
   for (int K = tid; K < nkeys; K += blockDim.x) {
     int run = 0;
-    for (int b0 = 0; b0 < nchunks; b0 += 8) {  // 8 loads in flight
-      int c[8];
+    for (int b0 = 0; b0 < nchunks; b0 += 32) {  // 32 loads in flight (a prefill call has 32 chunks)
+      int c[32];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = (b0 + u < nchunks) ? __ldcg(a.bcnt + (size_t)(b0 + u) * nkeys + K) : 0;
+      for (int u = 0; u < 32; ++u) c[u] = (b0 + u < nchunks) ? __ldcg(a.bcnt + (size_t)(b0 + u) * nkeys + K) : 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < 32; ++u)
         if (b0 + u < nchunks) {
           a.bcnt[(size_t)(b0 + u) * nkeys + K] = run;  // exclusive chunk base
           run += c[u];
@@ -606,58 +670,91 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   int nbar = 0;
   TG_STAMP(0);
   // ---- P1 router (+ reset of the GEMM counters of this call)
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
   TG_STAMP(8);
   const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
   {
-    const int nkp = router_nkp(a.d, a.E_r), KP = router_kpart(a.d, a.E_r), Epad = router_epad(a.E_r);
+    const int nkp = router_nkp(a.d, a.E_r), KP = router_kpart(a.d, a.E_r);
     RouterSmem R;
     R.ldw = KP / 2 + 4;
+    R.nbuf = router_nbuf(a.d, a.E_r, a.nkeys);
     R.wg = reinterpret_cast<uint32_t *>(fsm);
-    R.xt = R.wg + Epad * R.ldw;
-    R.part = reinterpret_cast<float *>(R.xt + kRouterRows * R.ldw);
+    R.xt = reinterpret_cast<uint32_t *>(fsm + router_wg_bytes(a.d, a.E_r));
+    R.red = reinterpret_cast<double *>(fsm + router_wg_bytes(a.d, a.E_r) + R.nbuf * router_xtile_bytes(a.d, a.E_r));
+    R.tail = reinterpret_cast<uint8_t *>(R.red);
     const int bpp = gridDim.x / nkp;  // blocks per K part
     const int kp = blockIdx.x % nkp, slot = blockIdx.x / nkp;
-    // chained (decode-sized calls): at most one router item per block, P1b-P3 run by
-    // the last arrivers; phased (prefill-sized): grid-stride phases between barriers,
-    // so no block serialises the top-k of many groups
+    // Block (kp, slot) runs items (group slot + i * bpp, part kp); its items stream through a
+    // cp.async ring of nbuf x tiles (the loads of the next items in flight during this one).
+    // Decode-sized calls (one item per block): no grid barrier until the receive layout — the
+    // block that delivers the last K part of a group runs its top-k, the one completing a
+    // chunk's last group ranks the chunk, the one completing the last chunk runs the count
+    // exchange (last-arriver chain, group_arrive).  Prefill-sized calls: grid-stride top-k and
+    // rank phases between barriers (a chain would pile the top-k of many groups on the blocks
+    // that happen to arrive last).
     const bool chain = ngroups <= bpp;
     if (slot < bpp && slot < ngroups) {
-      int it = 0;
-      for (int grp = slot; grp < ngroups; grp += bpp, ++it) {
+      const int nit = (ngroups - slot + bpp - 1) / bpp;
+      const int pre = min(R.nbuf, nit);
+      for (int i = 0; i < pre; ++i) router_issue(a, R, slot + i * bpp, kp, i, i == 0);
+      for (int it = 0; it < nit; ++it) {
+        const int grp = slot + it * bpp;
+        // this item's group has landed once at most (pending items - 1) newer groups remain
+        const int newer = min(R.nbuf, nit - it) - 1;
+        if (newer >= 3) cp_async_wait<3>();
+        else if (newer == 2) cp_async_wait<2>();
+        else if (newer == 1) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        __syncthreads();
         if (it < 5) TG_STAMP(20 + 2 * it);
-        router_item(a, R, grp, kp, it == 0);
+        router_compute(a, R, grp, kp, it % R.nbuf);
         if (it < 5) TG_STAMP(21 + 2 * it);
-        if (chain) group_arrive(a, rk, grp, nkp, ngroups, R.part);
+        __syncthreads();  // buffer it % nbuf is free again
+        if (it + R.nbuf < nit) router_issue(a, R, slot + (it + R.nbuf) * bpp, kp, it % R.nbuf, false);
+        if (chain) group_arrive(a, rk, grp, nkp, ngroups, reinterpret_cast<float *>(R.tail));
       }
     }
     // every CTA issues its share of the L2 prefetch, behind the router's own loads: the router
-    // CTAs after their item (and its top-k chain), the idle ones after a short delay
+    // CTAs after their items (and their top-k chains), the idle ones after a short delay
     if (!(slot < bpp && slot < ngroups)) __nanosleep(2000);
     l2_prefetch_share(a, blockIdx.x, gridDim.x);
     if (!chain) {
       const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
       grid_barrier_z(gbar, nbar++, a.err);
-      for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) group_topk(a, rk, grp, R.part);
+      for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) group_topk(a, rk, grp, reinterpret_cast<float *>(R.tail));
       TG_STAMP(12);
       grid_barrier_z(gbar, nbar++, a.err);
-      for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, reinterpret_cast<uint8_t *>(R.part));
+      for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, R.tail);
       TG_STAMP(13);
       grid_barrier_z(gbar, nbar++, a.err);
       if (blockIdx.x == 0) {
         TG_STAMP(1);
-        exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(R.part));
+        exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(R.tail));
         TG_STAMP(14);
       }
     } else if (ngroups == 0 && blockIdx.x == 0) {
       // no tokens: the count exchange still runs (peers wait for this rank's counts)
-      exchange_counts(a, 0, reinterpret_cast<int32_t *>(R.part));
+      exchange_counts(a, 0, reinterpret_cast<int32_t *>(R.tail));
     }
   }
   if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + blockIdx.x] = globaltimer_ns();
   grid_barrier_z(gbar, nbar++, a.err);
   TG_STAMP(3);
+  if (a.world == 1) {
+    // P4 at world == 1, layout half: every pair's receive row and origin, and the token of every
+    // row (the rows themselves are copied in row order beside the GEMM, dispatch_local_rows)
+    const int npairs = a.T * a.k;
+    int2 *meta = reinterpret_cast<int2 *>(a.sym[a.rank] + a.L.meta);
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
+      const int t = p / a.k, K = __ldcg(a.key + p);
+      const int pos = __ldcg(a.dbase + K) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K) + __ldcg(a.lrank + p);
+      a.dst_pos[p] = pos;
+      meta[pos] = make_int2(a.rank, p);
+      a.srcrow[pos] = t;
+    }
+    grid_barrier_z(gbar, nbar++, a.err);
+  }
 }
 
 // In-call failover (NEXT-1, §5.1 "the AW re-dispatches the affected
@@ -673,7 +770,7 @@ __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys 
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
   if (blockIdx.x == 0 && threadIdx.x == 0)
     *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_max; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
   int nbar = 0;
   const int npairs = a.T * a.k;
@@ -750,6 +847,31 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) 
   }
 }
 
+// P4 at world == 1, copy half (warps w of nw, grid-wide numbering, beside the GEMM roles):
+// routed rows in receive-row order, then the shared expert's rows, each row's token read from
+// srcrow; after each row the count of its token tile (the GEMM1 unit dependency group: the
+// TMA producer starts a tile's B loads once all its rows have landed) is released.  Row order
+// = the order the GEMM work list consumes the tiles, so the first units start after a few
+// rows, not after the whole dispatch.  grp_of(r, shared) -> token-tile group of a row.
+template <typename GroupOf>
+__device__ __forceinline__ void dispatch_local_rows(const CallArgs &a, int w, int nw, int nrecv, GroupOf grp_of) {
+  const int lane = threadIdx.x & 31, nch = a.d >> 3;
+  const int nsh = (a.Fsh > 0) ? a.T : 0;
+  uint4 *recv = reinterpret_cast<uint4 *>(a.sym[a.rank] + a.L.recv);
+  for (int r = w; r < nrecv + nsh; r += nw) {
+    const bool sh = r >= nrecv;
+    const int row = sh ? a.R_sh0 + (r - nrecv) : r;
+    const int t = sh ? r - nrecv : __ldcg(a.srcrow + r);
+    copy_row(recv + (size_t)row * nch, reinterpret_cast<const uint4 *>(a.x + (size_t)t * a.d), nch, lane);
+    fence_proxy_async_global();  // generic stores -> later TMA (async proxy) reads
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(a.rdy + grp_of(sh ? r - nrecv : r, sh), 1);
+    }
+  }
+}
+
 // Token dedup, receiving side: once every source's rows have landed, rows that a
 // source sent once for several of its pairs are copied locally into the other
 // pairs' positions.  Warps w of nw (grid-wide numbering); the caller counts the
@@ -784,12 +906,9 @@ __host__ __device__ inline size_t tg_max(size_t x, size_t y) { return x > y ? x 
 
 // Dynamic shared memory of the front phases (k_layer takes the max with the GEMM ring).
 __host__ __device__ inline size_t front_smem(const CallArgs &a) {
-  const int KP = router_kpart(a.d, a.E_r), ldw = KP / 2 + 4;
-  // R.wg + R.xt, then R.part: router warp partials, and in turn group top-k logits,
-  // the rank bitmap and the exchange arrays
-  const size_t topk = (size_t)kRouterRows * (a.E_r + 1) + kRouterRows * kMaxK;
-  const size_t part = tg_max(tg_max((size_t)8 * kRouterRows * 64, topk), (size_t)8 * a.nkeys);
-  return sizeof(uint32_t) * (size_t)(router_epad(a.E_r) + kRouterRows) * ldw + sizeof(float) * part;
+  // Wg slice + x-tile ring + scratch (router partials / group top-k / rank / exchange)
+  return router_wg_bytes(a.d, a.E_r) + router_nbuf(a.d, a.E_r, a.nkeys) * router_xtile_bytes(a.d, a.E_r) +
+         front_scratch_bytes(a.E_r, a.nkeys);
 }
 
 }  // namespace tg

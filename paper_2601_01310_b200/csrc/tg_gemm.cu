@@ -63,6 +63,82 @@ __device__ __forceinline__ float silu_f(float a) { return __fdiv_rn(a, 1.0f + ex
 
 __device__ __forceinline__ int box_index(int nrows) { return ((nrows + 15) >> 4) - 1; }
 
+// GK5 combine of NB chunks of 8 consecutive outputs (16-B chunks c8_0 + i * stride) of token t
+// (§2.1, R#5, R#16): out = bf16(sum_j w_j y_j (+ y_sh, or + sg * y_sh)) in fp32, fma chain
+// in slot order j.  The loads of two slots x NB chunks are in flight together (the combine is
+// bound by memory latency per thread, not by its arithmetic).
+template <int NB>
+__device__ __forceinline__ void combine_chunks(const CallArgs &a, const bf16 *ybuf, int t, int c8_0, int stride) {
+  const int nch = a.d >> 3;
+  float acc[NB][8];
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) acc[i][qq] = 0.f;
+  auto fma8 = [&](float (&ac)[8], const uint4 &v, float wj) {
+    const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      float2 f = __bfloat1622float2(vp[qq]);
+      ac[2 * qq] = __fmaf_rn(wj, f.x, ac[2 * qq]);
+      ac[2 * qq + 1] = __fmaf_rn(wj, f.y, ac[2 * qq + 1]);
+    }
+  };
+  for (int j = 0; j < a.k; j += 2) {
+    const bool two = j + 1 < a.k;
+    const float w0 = __ldcg(a.w + (size_t)t * a.k + j), w1 = two ? __ldcg(a.w + (size_t)t * a.k + j + 1) : 0.f;
+    uint4 v0[NB], v1[NB];
+    const uint4 *y0 = reinterpret_cast<const uint4 *>(ybuf + ((size_t)t * a.k + j) * a.d);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int c8 = c8_0 + i * stride;
+      if (c8 < nch) {
+        v0[i] = __ldcg(y0 + c8);
+        if (two) v1[i] = __ldcg(y0 + (a.d >> 3) + c8);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (c8_0 + i * stride < nch) {
+        fma8(acc[i], v0[i], w0);
+        if (two) fma8(acc[i], v1[i], w1);
+      }
+  }
+  if (a.Fsh > 0) {
+    const float sg = a.shared_gate ? __ldcg(a.sgate + t) : 1.f;
+    uint4 v[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (c8_0 + i * stride < nch) v[i] = __ldcg(reinterpret_cast<const uint4 *>(a.ysh + (size_t)t * a.d) + c8_0 + i * stride);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      if (c8_0 + i * stride >= nch) continue;
+      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&v[i]);
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        float2 f = __bfloat1622float2(vp[qq]);
+        if (a.shared_gate) {  // shared expert scaled by sigmoid(x . wsg)
+          acc[i][2 * qq] = __fmaf_rn(sg, f.x, acc[i][2 * qq]);
+          acc[i][2 * qq + 1] = __fmaf_rn(sg, f.y, acc[i][2 * qq + 1]);
+        } else {
+          acc[i][2 * qq] = __fadd_rn(acc[i][2 * qq], f.x);
+          acc[i][2 * qq + 1] = __fadd_rn(acc[i][2 * qq + 1], f.y);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const int c8 = c8_0 + i * stride;
+    if (c8 >= nch) continue;
+    uint4 o;
+    __nv_bfloat162 *op = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) op[qq] = __floats2bfloat162_rn(acc[i][2 * qq], acc[i][2 * qq + 1]);
+    reinterpret_cast<uint4 *>(a.out + (size_t)t * a.d)[c8] = o;
+  }
+}
+
 // Warp-parallel exclusive scan of per-slot quantities (lanes own contiguous slot ranges).
 __device__ void build_plan(const CallArgs &a, GemmShared *P) {
   const int lane = threadIdx.x & 31;
@@ -212,9 +288,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else front_phase(a, rk, smem_raw);
   // ===================== P4 dispatch (all warps; r01 A/B: 3.5% faster at 4 GPUs than on
   // warps 2-7 beside the first weight loads, equal at 1 GPU) =====================
-  dispatch_rows(a, blockIdx.x * 8 + (threadIdx.x >> 5), gridDim.x * 8);
-  __syncthreads();
-  if (threadIdx.x == 0) dispatch_done(a);
+  if (a.world > 1) {
+    dispatch_rows(a, blockIdx.x * 8 + (threadIdx.x >> 5), gridDim.x * 8);
+    __syncthreads();
+    if (threadIdx.x == 0) dispatch_done(a);
+  }
   if (a.inject_fail) return;  // fault injection (tests): crash after the dispatch, the peers hold the rows
   // the ring below is refilled by TMA (async proxy) after the front's generic smem writes
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -267,7 +345,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // stages get their A tiles at once and their token (B) tiles once every
       // source's rows have landed (release/acquire on per-source
       // epoch flags, then ordered before async-proxy reads).
-      bool data_ok = false;
+      bool data_ok = a.world == 1;  // world == 1: per-tile row counters instead (rdy)
       int npend = 0;  // pending token-tile loads, held by the lane that will issue them
       int pst[kStages], pkb[kStages], prow[kStages];
       uint32_t pab[kStages];
@@ -301,6 +379,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tma_load_2d(ring + pst[i] * stage_bytes + pab[i], pmap[i], &S->full[pst[i]], pkb[i] * BK, prow[i], pol_x);
         npend = 0;
       };
+      // world == 1: a unit's token rows are counted per tile (rdy); its pending B loads are
+      // issued once the count is complete
+      bool unit_ok = true;
+      int udep = 0, urows = 0;
+      auto wait_rows = [&]() {
+        if (lane == 0) wait_ctr_ge(a.rdy + udep, urows, err, 0x4005);
+        __syncwarp();
+        fence_proxy_async_global();
+        unit_ok = true;
+        for (int i = 0; i < npend; ++i)
+          tma_load_2d(ring + pst[i] * stage_bytes + pab[i], pmap[i], &S->full[pst[i]], pkb[i] * BK, prow[i], pol_x);
+        npend = 0;
+      };
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0;; ++it) {
@@ -323,6 +414,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const Unit U = decode_unit(a, S, u);
         const bool g1 = (U.kind == U_G1 || U.kind == U_G1_SH);
         const bool sh = (U.kind == U_G1_SH || U.kind == U_G2_SH);
+        if (g1 && a.world == 1) {
+          // the token tile's rows are copied beside the GEMM (dispatch_local_rows): B loads go
+          // out once they have landed, the unit's weight (A) tiles at once
+          int ok = 0;
+          if (lane == 0) ok = ld_acquire_gpu(a.rdy + U.dep) >= U.nrows;
+          unit_ok = __shfl_sync(0xffffffffu, ok, 0) != 0;
+          if (unit_ok) fence_proxy_async_global();
+          udep = U.dep;
+          urows = U.nrows;
+        }
         if (!g1) {
           if (!data_ok) wait_data();  // GEMM1 tiles waiting on pending B loads come first
           // all GEMM1 tiles of this (slot, n-tile) have written H
@@ -346,6 +447,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = U.kb0; kb < U.kb1; kb += kps) {
           const int cnt = min(kps, U.kb1 - kb);
           if (!data_ok && __any_sync(0xffffffffu, npend == nstages)) wait_data();  // every stage holds a pending B tile
+          if (!unit_ok && __any_sync(0xffffffffu, npend == nstages)) wait_rows();
           if (lane == 0) {
             mbar_wait(&S->empty[stage], phase ^ 1, err);
             mbar_arrive_expect_tx(&S->full[stage], (uint32_t)cnt * sub);
@@ -359,7 +461,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             } else if (role == 1) {
               if (g1) tma_load_2d(sb + kTileBytes, mA1, &S->full[stage], kk, rowA, pol_w);
               else if (U.dual) tma_load_2d(sb + kTileBytes, mA0, &S->full[stage], kk, rowA + BM, pol_w);
-            } else if (data_ok) {
+            } else if (data_ok && unit_ok) {
               tma_load_2d(sb + abytes, mB, &S->full[stage], kk, rowB, pol_x);
             } else {
               pst[npend] = stage; pkb[npend] = kb + li; prow[npend] = rowB;
@@ -369,6 +471,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (++stage == nstages) { stage = 0; phase ^= 1; }
         }
+        if (!unit_ok && __any_sync(0xffffffffu, npend > 0)) wait_rows();  // pending loads stay within a unit
+        unit_ok = true;
       }
     }
   } else if (warp == 1) {
@@ -435,6 +539,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
+    if (a.world == 1 && (warp == 2 || warp == 3)) {
+      // ===================== P4 at world == 1: rows copied in receive-row order (warps 2-3) =====================
+      dispatch_local_rows(a, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, S->nrecv, [&](int r, bool shr) {
+        if (shr) return S->goff[a.S_loc] + r / a.bn;
+        const int s = find_seg(S->rowoff, a.S_loc, r);
+        return S->goff[s] + (r - S->rowoff[s]) / a.bn;
+      });
+    }
     // ===================== token dedup, receiving side (warps 2-7, multi-GPU) =====================
     if (dedup) {
       if (lane == 0) {
@@ -609,6 +721,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           named_bar_sync(1, 128);
         }
+        if (a.world == 1 && (!split || S->red_last)) {
+          // per-token arrivals (one per unit storing a token's outputs): the combine below starts
+          // a token as soon as all k (+ shared) outputs over every c-tile are stored, without a
+          // grid barrier after the GEMM
+          if (sh) named_bar_sync(1, 128);  // every y_sh store of the unit done
+          __threadfence();
+          for (int i = et; i < U.nrows; i += 128)  // token tiles of up to 256 (wide mode)
+            atomicAdd(a.tokctr + (sh ? U.n0 - a.R_sh0 + i : meta[U.n0 + i].y / a.k), 1);
+        }
       }
       if (a.trace && et == 0) {
         uint32_t smid;
@@ -626,6 +747,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   // ===================== combine (GK5), all CTAs =====================
+  if (a.world == 1) {
+    // warp per token, grid-stride from this CTA's warps as soon as its GEMM work is done: a
+    // token is combined once its arrival count is complete (no grid barrier); a lane owns
+    // d / 256 chunks of 8 outputs, all their loads in flight
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int ctiles = (a.d + BM * (a.g2dual ? 2 : 1) - 1) / (BM * (a.g2dual ? 2 : 1));
+    const int target = (a.k + (a.Fsh > 0 ? 1 : 0)) * ctiles;
+    const bf16 *ybuf = reinterpret_cast<const bf16 *>(a.sym[a.rank] + a.L.ybuf);
+    for (int t = blockIdx.x * 8 + warp; t < a.T; t += gridDim.x * 8) {
+      if (lane == 0) wait_ctr_ge(a.tokctr + t, target, err, 0x5002);
+      __syncwarp();
+      __threadfence();
+      for (int c0 = lane; c0 < (a.d >> 3); c0 += 4 * 32) combine_chunks<4>(a, ybuf, t, c0, 32);
+    }
+    return;
+  }
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 10);
   grid_barrier(gbar, a.epoch, 1, 0, err);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -650,47 +787,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nch = a.d >> 3;
   const size_t total = (size_t)a.T * nch;
   const bf16 *ybuf = reinterpret_cast<const bf16 *>(a.sym[a.rank] + a.L.ybuf);
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int t = (int)(i / nch), c8 = (int)(i % nch);
-    float acc[8];
+  const size_t nthr = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += 4 * nthr) {
+    // four chunks (i, i + nthr, ...) per step, of up to four tokens
 #pragma unroll
-    for (int qq = 0; qq < 8; ++qq) acc[qq] = 0.f;
-    for (int j = 0; j < a.k; ++j) {
-      const float wj = __ldcg(a.w + (size_t)t * a.k + j);
-      uint4 v = __ldcg(reinterpret_cast<const uint4 *>(ybuf + ((size_t)t * a.k + j) * a.d) + c8);
-      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&v);
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        float2 f = __bfloat1622float2(vp[qq]);
-        acc[2 * qq] = __fmaf_rn(wj, f.x, acc[2 * qq]);
-        acc[2 * qq + 1] = __fmaf_rn(wj, f.y, acc[2 * qq + 1]);
-      }
+    for (int u = 0; u < 4; ++u) {
+      const size_t ii = i + u * nthr;
+      if (ii < total) combine_chunks<1>(a, ybuf, (int)(ii / nch), (int)(ii % nch), 0);
     }
-    if (a.Fsh > 0) {
-      uint4 v = __ldcg(reinterpret_cast<const uint4 *>(a.ysh + (size_t)t * a.d) + c8);
-      const __nv_bfloat162 *vp = reinterpret_cast<const __nv_bfloat162 *>(&v);
-      if (a.shared_gate) {  // shared expert scaled by sigmoid(x . wsg)
-        const float sg = __ldcg(a.sgate + t);
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          float2 f = __bfloat1622float2(vp[qq]);
-          acc[2 * qq] = __fmaf_rn(sg, f.x, acc[2 * qq]);
-          acc[2 * qq + 1] = __fmaf_rn(sg, f.y, acc[2 * qq + 1]);
-        }
-      } else {
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          float2 f = __bfloat1622float2(vp[qq]);
-          acc[2 * qq] = __fadd_rn(acc[2 * qq], f.x);
-          acc[2 * qq + 1] = __fadd_rn(acc[2 * qq + 1], f.y);
-        }
-      }
-    }
-    uint4 o;
-    __nv_bfloat162 *op = reinterpret_cast<__nv_bfloat162 *>(&o);
-#pragma unroll
-    for (int qq = 0; qq < 4; ++qq) op[qq] = __floats2bfloat162_rn(acc[2 * qq], acc[2 * qq + 1]);
-    reinterpret_cast<uint4 *>(a.out + (size_t)t * a.d)[c8] = o;
   }
   if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) a.trace[a.n_units_max + 148 + 17] = globaltimer_ns();
 }

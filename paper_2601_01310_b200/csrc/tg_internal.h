@@ -28,7 +28,7 @@ constexpr int BK = 64;
 constexpr int BN_MAX = 256;
 constexpr int kStages = 8;                      // maximum ring depth (stage size set per call)
 constexpr int kTileBytes = 16384;               // 128 rows x 128 B
-constexpr int kRingBytes = 214 * 1024;          // stage ring: floor(214 KB / stage) stages
+constexpr int kRingBytes = 208 * 1024;          // stage ring: floor(208 KB / stage) stages (4 x 48 KB, 3 x 64 KB)
 constexpr int BN_MAX_EPI = 256;                 // token-tile width bound of the GEMM2 epilogue table
 constexpr int kSchedDepth = 8;
 constexpr int kGemmThreads = 256;               // w0 TMA, w1 MMA, w2 TMEM, w4-7 epilogue
@@ -135,8 +135,12 @@ struct CallArgs {
                          // [6] ranks taking part in this run (alive and heard from in the count exchange);
                          // u64 grid barriers at [8], [10], [12]
   float *logits;         // [T_max][E_r] router logits of the last call (parity export; nullptr = off)
-  int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters
+  int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters, then rdy and tokctr
   int n_ctr_max;
+  int32_t *rdy;          // [n_grp_max] world == 1: rows of each token tile copied into recv
+  int32_t *tokctr;       // [T_max] world == 1: expert outputs (units) of each token stored
+  int n_ctr_all;         // ctr + rdy + tokctr entries (reset together at the start of a call)
+  int32_t *srcrow;       // [R_cap] world == 1: token of each received row
   int32_t *n_units;      // [1] units of the last call (written by the GEMM, diagnostics)
   int n_units_max;       // capacity bound (trace sizing)
   int *err;              // host-mapped error word
