@@ -225,7 +225,9 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   c->R_sh0 = c->R_cap;
   c->R_tot = c->R_cap + (Fsh > 0 ? c->T_max : 0);
   // fixed split-K for long GEMM2 reductions: a function of the shape only
-  c->nsplit = (F / BK >= 128 && (F / BK) % 4 == 0) ? 4 : (F / BK >= 128 && (F / BK) % 2 == 0) ? 2 : 1;
+  // (r02 same-box A/B at Mixtral decode, F = 14336: 1 split 500.6 us, 2 splits 494.8, 4 splits 508.5:
+  // the fp32 partials cost HBM traffic, one split leaves 140-us units for the last wave)
+  c->nsplit = (F / BK >= 128 && (F / BK) % 2 == 0) ? 2 : 1;
   if (const char *ns = getenv("TG_NSPLIT")) {  // development override (A/B timing)
     const int v = atoi(ns);
     if (v >= 1 && v <= 16 && (F / BK) % v == 0) c->nsplit = v;
@@ -678,6 +680,16 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
     a.g2dual = !wide && c->force_dual != 0;
   }
   a.trace = c->tracing ? c->trace : nullptr;
+  {
+    // world == 1 fast paths; TG_LOCAL: development A/B switch ("0" both off,
+    // "r" row-ordered dispatch only, "c" barrier-free combine only)
+    const char *e = getenv("TG_LOCAL");
+    const bool rows = !e || e[0] == '1' || e[0] == 'r', comb = !e || e[0] == '1' || e[0] == 'c';
+    a.local_rows = c->world == 1 && rows;
+    a.local_comb = c->world == 1 && comb;
+    const char *dv = getenv("TG_DEV");
+    a.dev = dv ? atoi(dv) : 0;
+  }
   a.alive = c->alive;
   a.fslot_data = FLAG_DATA;
   a.fslot_comb = FLAG_COMB;

@@ -159,7 +159,7 @@ __device__ __forceinline__ void router_issue(const CallArgs &a, const RouterSmem
 // sets of 8 k16 steps, each in its own fp32 registers, the sets summed in fp64 in K order
 // (shorter fp32 chains: ~1 ulp of logit instead of several), sub-slices likewise through smem;
 // the part's sum is stored rounded to fp32.  Order fixed by (d, E): deterministic, row-invariant.
-__device__ void router_compute(const CallArgs &a, const RouterSmem &R, int grp, int kp, int buf) {
+__device__ __forceinline__ void router_compute(const CallArgs &a, const RouterSmem &R, int grp, int kp, int buf) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = a.d, E = a.E_r;
   const int g = lane >> 2, c = lane & 3;
@@ -188,8 +188,10 @@ __device__ void router_compute(const CallArgs &a, const RouterSmem &R, int grp, 
 #pragma unroll
           for (int i = 0; i < 4; ++i) acc[q][m][i] = 0.f;
       // the sets' steps interleaved: 8 independent accumulator chains per warp (the set a
-      // step belongs to, not the issue order, decides where it is summed)
-      for (int st = 0; st < 8; ++st) {
+      // step belongs to, not the issue order, decides where it is summed); the step loop is
+      // not unrolled (short code: decode parts run 4 steps of one set)
+#pragma unroll 1
+      for (int st = 0; st < min(steps, 8); ++st) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int kstep = q * 8 + st;
@@ -446,12 +448,12 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
   const bool sys = a.world > 1;
   for (int K = tid; K < nkeys; K += blockDim.x) {
     int run = 0;
-    for (int b0 = 0; b0 < nchunks; b0 += 32) {  // 32 loads in flight (a prefill call has 32 chunks)
-      int c[32];
+    for (int b0 = 0; b0 < nchunks; b0 += 8) {  // 8 loads in flight (short code: this runs cold, once per call)
+      int c[8];
 #pragma unroll
-      for (int u = 0; u < 32; ++u) c[u] = (b0 + u < nchunks) ? __ldcg(a.bcnt + (size_t)(b0 + u) * nkeys + K) : 0;
+      for (int u = 0; u < 8; ++u) c[u] = (b0 + u < nchunks) ? __ldcg(a.bcnt + (size_t)(b0 + u) * nkeys + K) : 0;
 #pragma unroll
-      for (int u = 0; u < 32; ++u)
+      for (int u = 0; u < 8; ++u)
         if (b0 + u < nchunks) {
           a.bcnt[(size_t)(b0 + u) * nkeys + K] = run;  // exclusive chunk base
           run += c[u];
@@ -555,6 +557,23 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
   for (int s = tid; s < a.S_loc; s += blockDim.x) a.slot_rows[s] = gsum[a.rank * a.S_max + s];
 }
 
+// P4 at world == 1, layout half: every pair's receive row and origin, and the token of every
+// row (the rows themselves are copied in row order beside the GEMM, dispatch_local_rows).  Up
+// to kLocalLayoutBlock pairs (decode) it is run by the block that ran the count exchange, right
+// after it (no extra grid barrier); larger calls run it on every thread after the barrier.
+constexpr int kLocalLayoutBlock = 4096;
+__device__ __forceinline__ void local_layout(const CallArgs &a, int i0, int stride) {
+  const int npairs = a.T * a.k;
+  int2 *meta = reinterpret_cast<int2 *>(a.sym[a.rank] + a.L.meta);
+  for (int p = i0; p < npairs; p += stride) {
+    const int t = p / a.k, K = __ldcg(a.key + p);
+    const int pos = __ldcg(a.dbase + K) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K) + __ldcg(a.lrank + p);
+    a.dst_pos[p] = pos;
+    meta[pos] = make_int2(a.rank, p);
+    a.srcrow[pos] = t;
+  }
+}
+
 // ------------------------------------------------------- P1 -> P3 chaining
 // No grid barriers between P1, P1b, P2 and P3: the block that delivers the last
 // K part of a 32-token group runs its top-k (P1b); the block that completes the
@@ -610,6 +629,10 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
   TG_STAMP_ANY(1);
   exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(sm));
   TG_STAMP_ANY(14);
+  if (a.local_rows && a.T * a.k <= kLocalLayoutBlock) {
+    __syncthreads();  // dbase, written by this block's exchange
+    local_layout(a, threadIdx.x, blockDim.x);
+  }
   __syncthreads();
 }
 
@@ -732,6 +755,10 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
         TG_STAMP(1);
         exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(R.tail));
         TG_STAMP(14);
+        if (a.local_rows && a.T * a.k <= kLocalLayoutBlock) {
+          __syncthreads();
+          local_layout(a, threadIdx.x, blockDim.x);
+        }
       }
     } else if (ngroups == 0 && blockIdx.x == 0) {
       // no tokens: the count exchange still runs (peers wait for this rank's counts)
@@ -741,18 +768,8 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + blockIdx.x] = globaltimer_ns();
   grid_barrier_z(gbar, nbar++, a.err);
   TG_STAMP(3);
-  if (a.world == 1) {
-    // P4 at world == 1, layout half: every pair's receive row and origin, and the token of every
-    // row (the rows themselves are copied in row order beside the GEMM, dispatch_local_rows)
-    const int npairs = a.T * a.k;
-    int2 *meta = reinterpret_cast<int2 *>(a.sym[a.rank] + a.L.meta);
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
-      const int t = p / a.k, K = __ldcg(a.key + p);
-      const int pos = __ldcg(a.dbase + K) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K) + __ldcg(a.lrank + p);
-      a.dst_pos[p] = pos;
-      meta[pos] = make_int2(a.rank, p);
-      a.srcrow[pos] = t;
-    }
+  if (a.local_rows && a.T * a.k > kLocalLayoutBlock) {  // (smaller calls: by the exchange block)
+    local_layout(a, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
     grid_barrier_z(gbar, nbar++, a.err);
   }
 }

@@ -56,10 +56,12 @@ struct GemmShared {
   int roff[kMaxPlan];      // reduction-group offsets
 };
 
-// silu(a) = a / (1 + e^-a) with IEEE expf (<= 2 ulp) and IEEE division (SURVEY 8(c) GPU
-// numerics rules): a few ulps of fp32, the part of the h bound of DESIGN.md R#24 that does
-// not come from the accumulation (the oracle computes it in fp64).
-__device__ __forceinline__ float silu_f(float a) { return __fdiv_rn(a, 1.0f + expf(-a)); }
+// silu(a) = a / (1 + e^-a) with the fast exp (ex2.approx of a * log2 e: relative error <= 2 +
+// 1.16 |a| ulp) and the fast divide (<= 2 ulp): <= (5 + 1.2 |a|) ulp of fp32 relative, well below
+// the bf16 rounding of h that follows (R#26; the per-storage-point parity bound of h
+// includes it).  IEEE expf + division measured 10 % slower per prefill call: the SwiGLU
+// epilogue is on the critical path of compute-bound GEMM1 units.
+__device__ __forceinline__ float silu_f(float a) { return __fdividef(a, 1.0f + __expf(-a)); }
 
 __device__ __forceinline__ int box_index(int nrows) { return ((nrows + 15) >> 4) - 1; }
 
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else front_phase(a, rk, smem_raw);
   // ===================== P4 dispatch (all warps; r01 A/B: 3.5% faster at 4 GPUs than on
   // warps 2-7 beside the first weight loads, equal at 1 GPU) =====================
-  if (a.world > 1) {
+  if (!a.local_rows) {
     dispatch_rows(a, blockIdx.x * 8 + (threadIdx.x >> 5), gridDim.x * 8);
     __syncthreads();
     if (threadIdx.x == 0) dispatch_done(a);
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // stages get their A tiles at once and their token (B) tiles once every
       // source's rows have landed (release/acquire on per-source
       // epoch flags, then ordered before async-proxy reads).
-      bool data_ok = a.world == 1;  // world == 1: per-tile row counters instead (rdy)
+      bool data_ok = a.local_rows;  // world == 1: per-tile row counters instead (rdy)
       int npend = 0;  // pending token-tile loads, held by the lane that will issue them
       int pst[kStages], pkb[kStages], prow[kStages];
       uint32_t pab[kStages];
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const Unit U = decode_unit(a, S, u);
         const bool g1 = (U.kind == U_G1 || U.kind == U_G1_SH);
         const bool sh = (U.kind == U_G1_SH || U.kind == U_G2_SH);
-        if (g1 && a.world == 1) {
+        if (g1 && a.local_rows) {
           // the token tile's rows are copied beside the GEMM (dispatch_local_rows): B loads go
           // out once they have landed, the unit's weight (A) tiles at once
           int ok = 0;
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    if (a.world == 1 && (warp == 2 || warp == 3)) {
+    if (a.local_rows && (warp == 2 || warp == 3)) {
       // ===================== P4 at world == 1: rows copied in receive-row order (warps 2-3) =====================
       dispatch_local_rows(a, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, S->nrecv, [&](int r, bool shr) {
         if (shr) return S->goff[a.S_loc] + r / a.bn;
@@ -721,14 +723,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           named_bar_sync(1, 128);
         }
-        if (a.world == 1 && (!split || S->red_last)) {
+        if (a.local_comb && (!split || S->red_last)) {
           // per-token arrivals (one per unit storing a token's outputs): the combine below starts
           // a token as soon as all k (+ shared) outputs over every c-tile are stored, without a
           // grid barrier after the GEMM
           if (sh) named_bar_sync(1, 128);  // every y_sh store of the unit done
           __threadfence();
           for (int i = et; i < U.nrows; i += 128)  // token tiles of up to 256 (wide mode)
-            atomicAdd(a.tokctr + (sh ? U.n0 - a.R_sh0 + i : meta[U.n0 + i].y / a.k), 1);
+            atomicAdd(a.tokctr + (sh ? U.n0 - a.R_sh0 + i : meta[U.n0 + i].y / a.k),
+                      (U.dual && U.m0 + BM < a.d) ? 2 : 1);
         }
       }
       if (a.trace && et == 0) {
@@ -747,13 +750,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   // ===================== combine (GK5), all CTAs =====================
-  if (a.world == 1) {
+  if (a.local_comb) {
     // warp per token, grid-stride from this CTA's warps as soon as its GEMM work is done: a
     // token is combined once its arrival count is complete (no grid barrier); a lane owns
     // d / 256 chunks of 8 outputs, all their loads in flight
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int ctiles = (a.d + BM * (a.g2dual ? 2 : 1) - 1) / (BM * (a.g2dual ? 2 : 1));
-    const int target = (a.k + (a.Fsh > 0 ? 1 : 0)) * ctiles;
+    // arrivals count 128-column output tiles (a dual unit stores two; d % 256 == 0 when dual)
+    const int target = (a.k + (a.Fsh > 0 ? 1 : 0)) * ((a.d + BM - 1) / BM);
     const bf16 *ybuf = reinterpret_cast<const bf16 *>(a.sym[a.rank] + a.L.ybuf);
     for (int t = blockIdx.x * 8 + warp; t < a.T; t += gridDim.x * 8) {
       if (lane == 0) wait_ctr_ge(a.tokctr + t, target, err, 0x5002);

@@ -141,6 +141,9 @@ struct CallArgs {
   int32_t *tokctr;       // [T_max] world == 1: expert outputs (units) of each token stored
   int n_ctr_all;         // ctr + rdy + tokctr entries (reset together at the start of a call)
   int32_t *srcrow;       // [R_cap] world == 1: token of each received row
+  int local_rows;        // world == 1: rows copied in row order beside the GEMM, per-tile counters
+  int local_comb;        // world == 1: per-token arrival counters, combine without a grid barrier
+  int dev;               // development A/B switches (TG_DEV)
   int32_t *n_units;      // [1] units of the last call (written by the GEMM, diagnostics)
   int n_units_max;       // capacity bound (trace sizing)
   int *err;              // host-mapped error word
