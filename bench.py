@@ -20,6 +20,22 @@ its arithmetic intensity reaches first: algorithmic HBM bytes (or FLOPs) per
 launch / its mean event-timed duration, against MEASURED_PEAKS.json.
 `--impl reference` times the CPU oracle (the tier's reference arm) on a
 bounded sample of the same workload.
+
+The default (N = 1, configs[1]) line also carries the north star's other two
+numbers, measured in the same run on the same GPU:
+  "prefill":  the Qwen1.5-MoE-shaped layer (configs[4] shape: 60 experts
+              top-4), prefill batch T = 8192, against the bf16 tensor roof;
+  "failover": the EW-failover protocol (SURVEY 8(d), P:1257 for context) on
+              the Mixtral-shaped layer with 2 logical EWs and shadow replicas
+              (N = 1) or the bench layer's N EWs (N > 1): calls stream, then
+              every rank masks EW1 (tg_mask_worker) and NaN-poisons its slots;
+              host latency of the mask, reroute latency (mask call -> first
+              post-mask call complete), per-call latency before / after, calls
+              that errored, and how many post-mask outputs are bitwise those of
+              the same inputs before the mask.
+`cpu_baseline` adds the oracle on ONE core (sched_setaffinity to one CPU, one
+thread) next to the all-core run, with the CPU model, and checks that both
+runs give the same output bits.
 """
 from __future__ import annotations
 
@@ -199,7 +215,18 @@ def layer_algorithmic_flops(shape, R_local, T_local):
     return f
 
 
-def cpu_oracle_sample(shape, L_host, x_host, pl, n_tokens, n_threads):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_oracle_sample(shape, L_host, x_host, pl, n_tokens, n_threads, want_out=False):
     """Time the oracle (as it stands) on the first n_tokens of the batch: O1..O8."""
     import oracle
     oracle.build()
@@ -215,7 +242,104 @@ def cpu_oracle_sample(shape, L_host, x_host, pl, n_tokens, n_threads):
                      gate_mode=shape.gate_mode, wsg=wsg)
     dt = time.perf_counter() - t0
     assert r["rc"] == 0
+    if want_out:
+        return n_tokens / dt, dt, r["out"]
     return n_tokens / dt, dt
+
+
+def oracle_one_core(shape, L_host, x_host, pl, n_tokens):
+    """The oracle single-threaded and pinned to one CPU (taskset -c 0), on the first
+    n_tokens; restores this process's affinity afterwards."""
+    old = os.sched_getaffinity(0)
+    cpu0 = min(old)
+    os.sched_setaffinity(0, {cpu0})
+    try:
+        return cpu_oracle_sample(shape, L_host, x_host, pl, n_tokens, 1, want_out=True)
+    finally:
+        os.sched_setaffinity(0, old)
+
+
+def time_calls(tg, layer, xs, outs, stream, n, warm=5):
+    """Per-call device times (ms) of n tg_moe_layer calls, events around each call."""
+    for i in range(warm):
+        tg.tg_moe_layer(layer.ctx, xs[i % len(xs)], outs[i % len(xs)], stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    for i in range(n):
+        evs[i][0].record(stream)
+        rc = tg.tg_moe_layer(layer.ctx, xs[i % len(xs)], outs[i % len(xs)], stream)
+        if rc != tg.TG_OK:
+            raise tg.TarragonError(rc, tg.tg_last_error(layer.ctx))
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def prefill_record(tg, dev, seed, steps):
+    """North star: the prefill path against the bf16 tensor roof, on the Qwen1.5-MoE-shaped layer
+    (60 experts top-4, F 1408), T = 8192 tokens in one call, one B200."""
+    shape = wl.CONFIGS["qwen_prefill"]
+    pl = wl.make_placement(shape.E, 1, 1, shadows=False)
+    L = make_weights_device(shape, seed, dev, list(range(shape.E)))
+    layer = tg.MoELayer(shape, pl, L, max_tokens_per_rank=shape.T, device=dev.index)
+    xs = [wl.make_tokens(shape, seed + 17 * i, T=shape.T, device=dev) for i in range(4)]
+    outs = [torch.empty_like(xs[0]) for _ in range(4)]
+    stream = torch.cuda.current_stream()
+    with ClockSampler(dev.index) as clk:
+        ts = time_calls(tg, layer, xs, outs, stream, steps, warm=10)
+    rt = layer.routing(shape.T)
+    R = int(rt["counts"].cpu().numpy()[0].sum())
+    flops = layer_algorithmic_flops(shape, R, shape.T)
+    ms = float(np.median(ts))
+    _, tf_burst, tf_sus, src = peaks()
+    tfs = flops / (ms / 1e3) / 1e12
+    layer.close()
+    del L, xs, outs
+    torch.cuda.empty_cache()
+    return {"workload": "BASELINE configs[4] shape: qwen_prefill (d=2048, E=60, top-4, F=1408), T=8192, 1 B200",
+            "us_per_call": ms * 1e3, "us_per_call_p95": float(np.percentile(ts, 95)) * 1e3,
+            "tokens_per_s": shape.T / (ms / 1e3), "calls": len(ts),
+            "algorithmic_flops_per_call": flops, "achieved_TFLOPs": tfs,
+            "roofline": {"bound": "tensor", "peak": tf_sus, "unit": "TFLOP/s", "frac": tfs / tf_sus,
+                         "peak_source": src + " (bf16 sustained)",
+                         "frac_of_burst": tfs / tf_burst, "frac_of_nominal_2250": tfs / 2250.0},
+            "north_star_bar": ">= 0.5 of bf16 peak", "clocks": clk.summary()}
+
+
+def failover_record(tg, layer, shape, xs, stream, N, rank, dev, n_calls=40):
+    """SURVEY 8(d) EW-failover protocol (BASELINE metric's second half): calls stream with
+    rotating inputs, then every rank masks EW1 (tg_mask_worker) and NaN-poisons its slots on its
+    rank; the next call is the reroute.  Returns latencies and the bit-identity count."""
+    pl = layer.pl
+    outs_pre = [torch.empty_like(xs[0]) for _ in xs]
+    pre = time_calls(tg, layer, xs, outs_pre, stream, n_calls)
+    ref = [o.clone() for o in outs_pre]
+    if N > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rc = tg.tg_mask_worker(layer.ctx, 1, 1)
+    t_mask = time.perf_counter() - t0
+    outs_post = [torch.empty_like(xs[0]) for _ in xs]
+    rc2 = tg.tg_moe_layer(layer.ctx, xs[0], outs_post[0], stream)
+    torch.cuda.synchronize()
+    t_reroute = time.perf_counter() - t0
+    # fail-stop semantics: nothing may read the masked EW's memory any more
+    if pl.ew_rank[1] == rank:
+        nan = torch.full((shape.F, shape.d), float("nan"), dtype=torch.bfloat16, device=dev)
+        nan2 = torch.full((shape.d, shape.F), float("nan"), dtype=torch.bfloat16, device=dev)
+        for sl, e in enumerate(pl.hosted[1]):
+            if e >= 0:
+                tg.tg_load_experts(layer.ctx, 1, sl, e, nan, nan, nan2)
+    if N > 1:
+        torch.distributed.barrier()
+    post = time_calls(tg, layer, xs, outs_post, stream, n_calls, warm=0)
+    ident = sum(int(torch.equal(a.view(torch.int16), b.view(torch.int16))) for a, b in zip(ref, outs_post))
+    errors = int(rc not in (tg.TG_OK,)) + int(rc2 != tg.TG_OK)
+    return {"protocol": "SURVEY 8(d): mask EW1 on every rank mid-stream, NaN-poison its slots",
+            "ews": pl.n_ews, "ranks": N, "mask_host_us": t_mask * 1e6, "reroute_ms": t_reroute * 1e3,
+            "pre_us_per_call": float(np.median(pre)) * 1e3, "post_us_per_call": float(np.median(post)) * 1e3,
+            "calls_errored": errors, "post_mask_outputs_bit_identical": ident, "post_mask_outputs_compared": len(ref),
+            "paper_context": "EW-failure stall ~0.3 s on H200 + RDMA (P:1257), not comparable hardware"}
 
 
 def main():
@@ -273,7 +397,8 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                                 "sample": f"first {n} of the batch's tokens, full O1-O8 per step"},
+                                 "sample": f"first {n} of the batch's tokens, full O1-O8 per step",
+                                 "cpu_model": cpu_model()},
                 "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -396,6 +521,21 @@ def main():
             "profiled_ms_per_step": ms_prof / args.steps,
             "per_kernel_ms": kt}
 
+    # ---- north star's other numbers (same run, same GPU)
+    prefill = None
+    if N == 1 and cfg != "qwen_prefill":
+        prefill = prefill_record(tg, dev, args.seed, 50)
+    fo_layer, fo_xs = layer, xs
+    if N == 1:  # 2 logical EWs with shadow replicas on the one GPU
+        pl2 = wl.make_placement(shape.E, 2, 1, shadows=True)
+        L2 = make_weights_device(shape, args.seed, dev, list(range(shape.E)))
+        fo_layer = tg.MoELayer(shape, pl2, L2, max_tokens_per_rank=T_r, device=local)
+    failover = failover_record(tg, fo_layer, shape, fo_xs, stream, N, rank, dev)
+    if fo_layer is not layer:
+        fo_layer.close()
+        del L2
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
         n = args.cpu_sample or 16
@@ -408,9 +548,16 @@ def main():
             # scale the sample to ~12 s of CPU work (bounded by the batch)
             n = int(min(xc.shape[0], max(n, n * 12.0 / max(dt, 1e-3))))
             v, dt = cpu_oracle_sample(shape, Lh, xc, pl, n, cores)
+        n1 = min(n, 8)
+        v1, dt1, out1 = oracle_one_core(shape, Lh, xc, pl, n1)
+        _, _, outa = cpu_oracle_sample(shape, Lh, xc, pl, n1, cores, want_out=True)
         cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                "sample": f"first {n} tokens of the bench batches through O1-O8 (fp64, {cores} threads over tokens), "
-                         f"{dt:.1f} s"}
+                         f"{dt:.1f} s",
+               "cpu_model": cpu_model(), "nproc": cores,
+               "one_core": {"value": v1, "unit": "tokens/s", "cores": 1, "pinned": "sched_setaffinity to one CPU",
+                            "sample": f"first {n1} tokens, {dt1:.1f} s",
+                            "bits_equal_to_all_core_run": bool(np.array_equal(out1, outa))}}
 
     if rank == 0:
         line = {"metric": "MoE-layer tokens/s", "value": value, "unit": "tokens/s", "n_gpus": N,
@@ -420,7 +567,7 @@ def main():
                 "clocks": clk.summary(), "gpu_launches": launches,
                 "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": T_glob * shape.d * 2,
                         "d2h_bytes_per_step": T_glob * shape.d * 2},
-                "roofline": roof, "cpu_baseline": cpu}
+                "roofline": roof, "cpu_baseline": cpu, "prefill": prefill, "failover": failover}
         print(json.dumps(line), flush=True)
     layer.close()
     if N > 1:

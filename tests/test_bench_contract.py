@@ -38,3 +38,9 @@ def test_bench_gpu_line():
     r = d["roofline"]
     assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] < 1.2
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    # the north star's other numbers in the same line
+    p = d["prefill"]
+    assert p["roofline"]["bound"] == "tensor" and 0 < p["roofline"]["frac"] < 1.2 and p["us_per_call"] > 0
+    f = d["failover"]
+    assert f["calls_errored"] == 0 and f["post_mask_outputs_bit_identical"] == f["post_mask_outputs_compared"]
+    assert f["mask_host_us"] > 0 and f["reroute_ms"] > 0
