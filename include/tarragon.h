@@ -103,17 +103,24 @@ tg_status tg_get_peer_handle(tg_ctx *ctx, void *out);
 tg_status tg_connect_peers(tg_ctx *ctx, const void *all_handles);
 
 /* Virtual ranks on one GPU (tests, and a GPU shared by several AW/EW
- * shards): ctxs[q] (q < world) are the ctxs of ranks 0..world-1, created in
- * this process on the SAME device; tg_connect_local(ctx, ctxs) maps them as
- * ctx's peers by device pointer (the data plane is the same code as over
+ * shards): ctxs[q] (q < world <= 4) are the ctxs of ranks 0..world-1, created
+ * in this process on the SAME device; tg_connect_local(ctx, ctxs) maps them
+ * as ctx's peers by device pointer (the data plane is the same code as over
  * NVLink: stores into peer regions, epoch flags).  Layout signatures must
- * match (TG_ERR_PEER).  tg_set_launch_ctas(ctx, n) (before the first call)
- * sets the CTAs of each launch: 0 = one per SM (default, cooperative launch);
- * 0 < n < SM count = a share of the GPU — the ranks' calls must then be
- * enqueued on different streams and their shares must add up to at most the
- * SM count, so that every rank's grid is resident at once.                */
+ * match (TG_ERR_PEER).  The ranks of a call wait on one another's flags, so
+ * they run as ONE cooperative launch, each rank on SM count / world CTAs:
+ * tg_moe_layer_multi(ctxs, world, x[], out[], n_tokens[], stream) is one
+ * tg_moe_layer call of every rank (n_tokens[r] < 0: rank r does not take part,
+ * as a rank that died before the call), and tg_failover_multi(ctxs, world,
+ * x[], out[], n_tokens[], stream, failed[]) is tg_failover of every rank that
+ * saw a failure (failed[r] = its failed-rank mask), in one launch.  Errors as
+ * tg_moe_layer / tg_failover; TG_ERR_INVALID if the ctxs are not ranks
+ * 0..world-1 of one device, TG_ERR_PEER if not connected by tg_connect_local. */
 tg_status tg_connect_local(tg_ctx *ctx, tg_ctx *const *ctxs);
-tg_status tg_set_launch_ctas(tg_ctx *ctx, int n_ctas);
+tg_status tg_moe_layer_multi(tg_ctx *const *ctxs, int world, const void *const *x, void *const *out,
+                             const int *n_tokens, void *stream);
+tg_status tg_failover_multi(tg_ctx *const *ctxs, int world, const void *const *x, void *const *out,
+                            const int *n_tokens, void *stream, uint32_t *failed);
 
 /* Router weights Wg [E][d] bf16 (host or device source; copied).  SPMD.
  * The gating network of P:265 §2.1 ("a gating network ... selects the top-k

@@ -48,7 +48,8 @@ _SIG = {
     "tg_get_peer_handle": ([_P, _P], _I),
     "tg_connect_peers": ([_P, _P], _I),
     "tg_connect_local": ([_P, _P], _I),
-    "tg_set_launch_ctas": ([_P, _I], _I),
+    "tg_moe_layer_multi": ([_P, _I, _P, _P, _P, _P], _I),
+    "tg_failover_multi": ([_P, _I, _P, _P, _P, _P, _P], _I),
     "tg_set_stage_export": ([_P, _I], _I),
     "tg_get_stage": ([_P, _I, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)], _I),
     "tg_load_gate": ([_P, _P, _I], _I),
@@ -160,8 +161,26 @@ def tg_connect_local(ctx, ctxs):
     _check(ctx, _lib.tg_connect_local(ctx, arr), "tg_connect_local")
 
 
-def tg_set_launch_ctas(ctx, n: int):
-    _check(ctx, _lib.tg_set_launch_ctas(ctx, int(n)), "tg_set_launch_ctas")
+def _ptrs(seq):
+    return (_P * len(seq))(*[(c.value if isinstance(c, _P) else c) for c in seq])
+
+
+def tg_moe_layer_multi(ctxs, xs, outs, stream=None) -> int:
+    """One call of every virtual rank of one GPU in one launch; xs[r] None = rank r absent."""
+    n = len(ctxs)
+    T = (ctypes.c_int * n)(*[(-1 if x is None else x.shape[0]) for x in xs])
+    return _lib.tg_moe_layer_multi(_ptrs(ctxs), n, _ptrs([_ptr(x) or 0 for x in xs]),
+                                   _ptrs([_ptr(o) or 0 for o in outs]), T, _stream(stream))
+
+
+def tg_failover_multi(ctxs, xs, outs, stream=None):
+    """tg_failover of every virtual rank in one launch: (status, [failed-rank mask per rank])."""
+    n = len(ctxs)
+    T = (ctypes.c_int * n)(*[(-1 if x is None else x.shape[0]) for x in xs])
+    f = (ctypes.c_uint32 * n)()
+    rc = _lib.tg_failover_multi(_ptrs(ctxs), n, _ptrs([_ptr(x) or 0 for x in xs]),
+                                _ptrs([_ptr(o) or 0 for o in outs]), T, _stream(stream), f)
+    return rc, list(f)
 
 
 def tg_set_stage_export(ctx, on=True):
@@ -371,7 +390,7 @@ class MoELayer:
     """
 
     def __init__(self, shape, placement, weights, max_tokens_per_rank, rank=0, world=1, device=None,
-                 group=None, version=1, _peers=None, launch_ctas=0):
+                 group=None, version=1, _peers=None):
         self.shape, self.pl = shape, placement
         self.rank, self.world = rank, world
         self.stage_export = False
@@ -380,8 +399,6 @@ class MoELayer:
                            placement.slots_per_ew, max_tokens_per_rank, rank, world, self.device,
                            d_ffn_shared=shape.F_sh, gate_mode=getattr(shape, "gate_mode", 0),
                            shared_gate=getattr(shape, "shared_gate", 0))
-        if launch_ctas:
-            tg_set_launch_ctas(self.ctx, launch_ctas)
         if _peers is not None:
             _peers.append(self.ctx)
             if len(_peers) == world:  # the last virtual rank connects everyone
@@ -466,32 +483,30 @@ class MoELayer:
             pass
 
 
-def local_ranks(shape, placement, weights, max_tokens_per_rank, world, device=None, n_sms=None):
-    """``world`` virtual ranks of one layer on ONE GPU (tests / driver evidence of the
-    multi-rank data plane): ctxs connected by device pointer (tg_connect_local), each
-    launching on n_sms // world CTAs.  Their calls must be enqueued on different
-    streams (``call_all``)."""
+def local_ranks(shape, placement, weights, max_tokens_per_rank, world, device=None):
+    """``world`` (<= 4) virtual ranks of one layer on ONE GPU (tests / driver evidence of the
+    multi-rank data plane): ctxs connected by device pointer (tg_connect_local); their calls
+    run as one cooperative launch (``call_all``: tg_moe_layer_multi)."""
     device = torch.cuda.current_device() if device is None else device
-    n_sms = n_sms or torch.cuda.get_device_properties(device).multi_processor_count
     peers = []
     layers = [None] * world
     # every ctx must exist before any is connected: create, then load (connect happens on the last init)
     for r in range(world):
         layers[r] = MoELayer(shape, placement, weights, max_tokens_per_rank, rank=r, world=world, device=device,
-                             _peers=peers, launch_ctas=n_sms // world)
+                             _peers=peers)
     return layers
 
 
-def call_all(layers, xs, outs=None, streams=None, skip=()):
-    """One tg_moe_layer call of every virtual rank (rank r on streams[r]); ranks in ``skip`` do
-    not call (a rank that died before the call).  Returns the statuses; does not synchronise."""
-    streams = streams or [torch.cuda.Stream() for _ in layers]
+def call_all(layers, xs, outs=None, stream=None, skip=()):
+    """One tg_moe_layer call of every virtual rank, as ONE launch; ranks in ``skip`` do not take
+    part (a rank that died before the call).  Returns (status, outs); does not synchronise."""
     outs = outs or [torch.empty_like(x) for x in xs]
-    rcs = []
-    for r, (L, x, o, st) in enumerate(zip(layers, xs, outs, streams)):
-        if r in skip:
-            rcs.append(None)
-            continue
-        st.wait_stream(torch.cuda.current_stream())
-        rcs.append(tg_moe_layer(L.ctx, x, o, st))
-    return rcs, outs, streams
+    xs2 = [None if r in skip else x for r, x in enumerate(xs)]
+    rc = tg_moe_layer_multi([l.ctx for l in layers], xs2, outs, stream)
+    return rc, outs
+
+
+def failover_all(layers, xs, outs, stream=None, skip=()):
+    """tg_failover of every virtual rank (except ``skip``), as one launch."""
+    xs2 = [None if r in skip else x for r, x in enumerate(xs)]
+    return tg_failover_multi([l.ctx for l in layers], xs2, outs, stream)

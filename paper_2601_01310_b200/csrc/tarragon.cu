@@ -68,7 +68,6 @@ struct tg_ctx {
   // ---- device
   bool host_only = true;
   int n_sms = 148;
-  int n_ctas = 0;                         // CTAs per launch (0 = one per SM); < n_sms: GPU shared by virtual ranks
   bool stage_export = false;              // parity export of the router logits (tg_set_stage_export)
   float *logits = nullptr;                // [T_max][E_r]
   bf16 *bank_w1 = nullptr, *bank_w3 = nullptr, *bank_w2 = nullptr, *wg = nullptr;
@@ -80,6 +79,7 @@ struct tg_ctx {
   void *scratch = nullptr;
   CallArgs args{};
   TmaMaps maps{};
+  TmaMaps *maps_dev = nullptr;            // device copy (fused launches of virtual ranks)
   int *err_host = nullptr, *err_dev = nullptr;
   uint64_t *trace = nullptr;                     // device trace buffer (diagnostics)
   bool tracing = false;
@@ -128,6 +128,13 @@ static tg_status fail(tg_ctx *c, tg_status s, const char *fmt, ...) {
   if (c && s == TG_ERR_CUDA) c->sticky = true;
   return s;
 }
+
+#define CK2(ctx, call)                                                                               \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) return fail(ctx, TG_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                          \
+  } while (0)
 
 #define CK(call)                                                                                     \
   do {                                                                                               \
@@ -377,6 +384,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
       c->maps.hs[i] = c->maps.h[i];
     }
   }
+  CKI(cudaMalloc(&c->maps_dev, sizeof(TmaMaps)));
+  CKI(cudaMemcpy(c->maps_dev, &c->maps, sizeof(TmaMaps), cudaMemcpyHostToDevice));
   CKI(layer_configure());
   CKI(cudaDeviceSynchronize());
 #undef CKI
@@ -455,15 +464,6 @@ tg_status tg_connect_local(tg_ctx *c, tg_ctx *const *ctxs) {
       return fail(c, TG_ERR_PEER, "rank %d's peer-visible region has another layout", q);
   }
   for (int q = 0; q < c->world; ++q) c->peer[q] = ctxs[q]->sym;
-  return TG_OK;
-}
-
-tg_status tg_set_launch_ctas(tg_ctx *c, int n) {
-  if (!c) return TG_ERR_INVALID;
-  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx");
-  if (n < 0 || n > c->n_sms) return fail(c, TG_ERR_INVALID, "launch CTAs %d not in [0, %d]", n, c->n_sms);
-  if (c->epoch != 0) return fail(c, TG_ERR_INVALID, "tg_set_launch_ctas must precede the first call");
-  c->n_ctas = (n == c->n_sms) ? 0 : n;
   return TG_OK;
 }
 
@@ -697,6 +697,9 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
   a.fail_timeout_ns = c->fail_timeout_ns;
   a.cnt_timeout_ns = c->cnt_timeout_ns;
   a.logits = c->stage_export ? c->logits : nullptr;
+  a.cta0 = 0;
+  a.ncta = c->n_sms;
+  a.absent = 0;
   a.replay = 0;
   a.failed = 0;
   a.key_old = nullptr;
@@ -705,7 +708,8 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
   return a;
 }
 
-tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream) {
+// Validation and per-call arguments of one rank's layer call (everything but the launch).
+static tg_status prepare_call(tg_ctx *c, const void *x, void *out, int T, CallArgs *a, RouteKeys *rk) {
   if (!c) return TG_ERR_INVALID;
   if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device): no compute path");
   tg_status st = check_sticky(c);
@@ -722,22 +726,77 @@ tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream)
   if (c->no_route) return fail(c, TG_ERR_NO_ROUTE, "some expert has no unmasked candidate: nothing launched");
   for (int q = 0; q < c->world; ++q)
     if (!c->peer[q] && ((c->alive >> q) & 1u)) return fail(c, TG_ERR_PEER, "peer %d not connected (tg_connect_peers)", q);
+  *a = call_args(c, T, x, out, rk);
+  a->xepoch = ++c->xepoch;
+  a->fepoch = a->xepoch;
+  a->cnt_buf = (int)(a->xepoch & 1);
+  a->inject_fail = c->inject_next ? 1 : 0;
+  c->inject_next = false;
+  return TG_OK;
+}
+
+tg_status tg_moe_layer(tg_ctx *c, const void *x, void *out, int T, void *stream) {
+  CallArgs a;
+  RouteKeys rk;
+  tg_status st = prepare_call(c, x, out, T, &a, &rk);
+  if (st) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(c->device));
-  RouteKeys rk;
-  CallArgs a = call_args(c, T, x, out, &rk);
-  a.xepoch = ++c->xepoch;
-  a.fepoch = a.xepoch;
-  a.cnt_buf = (int)(a.xepoch & 1);
-  a.inject_fail = c->inject_next ? 1 : 0;
-  c->inject_next = false;
   c->n_ev = 0;
   rec(c, s);
-  CK(launch_layer(a, rk, c->maps, c->n_ctas ? c->n_ctas : c->n_sms, c->n_ctas != 0, s));
+  CK(launch_layer(a, rk, c->maps, c->n_sms, s));
   rec(c, s);
   if (c->prof) ++c->prof_calls;
   c->last_T = T;
   c->last_launches = 1;
+  return TG_OK;
+}
+
+// Virtual ranks of one GPU: one cooperative launch over every rank's data (their waits on one
+// another need them co-resident; separate launches carry no such guarantee).
+static tg_status check_multi(tg_ctx *const *ctxs, int n) {
+  if (!ctxs || n < 1 || n > kMaxVirt) return TG_ERR_INVALID;
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r] || ctxs[r]->host_only) return TG_ERR_INVALID;
+    if (ctxs[r]->rank != r || ctxs[r]->world != n || ctxs[r]->device != ctxs[0]->device)
+      return fail(ctxs[r], TG_ERR_INVALID, "fused launch: ctxs[%d] must be rank %d of %d on device %d", r, r, n,
+                  ctxs[0]->device);
+    if (ctxs[r]->peer[(r + 1) % n] != ctxs[(r + 1) % n]->sym)
+      return fail(ctxs[r], TG_ERR_PEER, "fused launch: ranks not connected by tg_connect_local");
+  }
+  return TG_OK;
+}
+
+tg_status tg_moe_layer_multi(tg_ctx *const *ctxs, int n, const void *const *x, void *const *out, const int *T,
+                             void *stream) {
+  tg_status st = check_multi(ctxs, n);
+  if (st) return st;
+  if (!x || !out || !T) return TG_ERR_INVALID;
+  static MultiArgs m;  // host staging of the kernel parameter (not thread-safe, as the ctxs)
+  memset(&m, 0, sizeof m);
+  m.n = n;
+  m.nper = ctxs[0]->n_sms / n;
+  for (int r = 0; r < n; ++r) {
+    tg_ctx *c = ctxs[r];
+    if (T[r] < 0) {  // does not take part (a rank that died before the call)
+      m.a[r].absent = 1;
+      continue;
+    }
+    st = prepare_call(c, x[r], out[r], T[r], &m.a[r], &m.rk[r]);
+    if (st) return st;
+    m.a[r].cta0 = r * m.nper;
+    m.a[r].ncta = m.nper;
+    m.a[r].pdl = 0;
+    m.maps[r] = c->maps_dev;
+  }
+  tg_ctx *c = ctxs[0];
+  CK(cudaSetDevice(c->device));
+  CK(launch_layer_multi(m, reinterpret_cast<cudaStream_t>(stream)));
+  for (int r = 0; r < n; ++r)
+    if (T[r] >= 0) {
+      ctxs[r]->last_T = T[r];
+      ctxs[r]->last_launches = 1;
+    }
   return TG_OK;
 }
 
@@ -755,15 +814,11 @@ tg_status tg_inject_failure(tg_ctx *c) {
   return TG_OK;
 }
 
-tg_status tg_failover(tg_ctx *c, const void *x, void *out, int T, void *stream, uint32_t *failed) {
-  if (!c) return TG_ERR_INVALID;
-  if (failed) *failed = 0;
-  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device): no compute path");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  CK(cudaSetDevice(c->device));
-  CK(cudaStreamSynchronize(s));
-  tg_status st = check_sticky(c);
-  if (st) return st;
+// In-call failover, host half: if the last call saw a peer fail, fail-stop the failed ranks and
+// build the replay run's arguments.  *fm_out = failed ranks (0: nothing to replay).
+static tg_status replay_args(tg_ctx *c, const void *x, void *out, int T, CallArgs *a, RouteKeys *rk,
+                             uint32_t *fm_out) {
+  *fm_out = 0;
   volatile int *hw = reinterpret_cast<volatile int *>(c->err_host);
   const uint32_t fm = static_cast<uint32_t>(hw[4]) & ~(1u << c->rank) & c->alive;
   if (!fm) return TG_OK;  // the last call saw no peer failure: nothing to do
@@ -778,34 +833,99 @@ tg_status tg_failover(tg_ctx *c, const void *x, void *out, int T, void *stream, 
         if (c->ew_rank[w] == q) c->mask[w] = 1;
     }
   resolve(c);
-  if (failed) *failed = fm;
+  *fm_out = fm;
   // ... and the pairs this rank had sent them are re-dispatched to the next live candidate
   // of their expert, on whichever surviving rank it lives: a replay run of k_layer in which
   // every survivor takes part (the survivors all saw the failure in the same call: each
   // waits for every live rank's combine flag), with its own flags and count buffer
-  RouteKeys rk;
-  CallArgs a = call_args(c, T, x, out, &rk);
-  a.xepoch = c->xepoch;
-  a.fepoch = ++c->rxepoch;
-  a.fslot_data = FLAG_RDATA;
-  a.fslot_comb = FLAG_RCOMB;
-  a.fslot_cnt = FLAG_RCNT;
-  a.cnt_buf = kCntBufReplay;
-  a.replay = 1;
-  a.failed = fm;
-  a.key_old = c->key_main;
-  a.key = c->key_replay;
-  a.logits = nullptr;
-  CK(launch_layer(a, rk, c->maps, c->n_ctas ? c->n_ctas : c->n_sms, c->n_ctas != 0, s));
-  CK(cudaStreamSynchronize(s));
-  st = check_sticky(c);
+  *a = call_args(c, T, x, out, rk);
+  a->xepoch = c->xepoch;
+  a->fepoch = ++c->rxepoch;
+  a->fslot_data = FLAG_RDATA;
+  a->fslot_comb = FLAG_RCOMB;
+  a->fslot_cnt = FLAG_RCNT;
+  a->cnt_buf = kCntBufReplay;
+  a->replay = 1;
+  a->failed = fm;
+  a->key_old = c->key_main;
+  a->key = c->key_replay;
+  a->logits = nullptr;
+  a->local_rows = 0;  // a replay is a multi-rank run (world > 1)
+  a->local_comb = 0;
+  return TG_OK;
+}
+
+static tg_status replay_status(tg_ctx *c) {
+  tg_status st = check_sticky(c);
   if (st) return st;
+  volatile int *hw = reinterpret_cast<volatile int *>(c->err_host);
   c->last_launches = 1;
   if (hw[5] > 0)
     return fail(c, TG_ERR_NO_ROUTE, "%d pairs have no live candidate left: not recomputed (their tokens' "
                 "outputs are incomplete)", hw[5]);
   if (static_cast<uint32_t>(hw[4]) & ~(1u << c->rank) & c->alive)
     return fail(c, TG_ERR_PEER, "another rank failed during the replay (call tg_failover again)");
+  return TG_OK;
+}
+
+tg_status tg_failover(tg_ctx *c, const void *x, void *out, int T, void *stream, uint32_t *failed) {
+  if (!c) return TG_ERR_INVALID;
+  if (failed) *failed = 0;
+  if (c->host_only) return fail(c, TG_ERR_UNSUPPORTED, "host-only ctx (no CUDA device): no compute path");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(s));
+  tg_status st = check_sticky(c);
+  if (st) return st;
+  CallArgs a;
+  RouteKeys rk;
+  uint32_t fm = 0;
+  if ((st = replay_args(c, x, out, T, &a, &rk, &fm))) return st;
+  if (failed) *failed = fm;
+  if (!fm) return TG_OK;
+  CK(launch_layer(a, rk, c->maps, c->n_sms, s));
+  CK(cudaStreamSynchronize(s));
+  return replay_status(c);
+}
+
+tg_status tg_failover_multi(tg_ctx *const *ctxs, int n, const void *const *x, void *const *out, const int *T,
+                            void *stream, uint32_t *failed) {
+  tg_status st = check_multi(ctxs, n);
+  if (st) return st;
+  if (!x || !out || !T || !failed) return TG_ERR_INVALID;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK2(ctxs[0], cudaSetDevice(ctxs[0]->device));
+  CK2(ctxs[0], cudaStreamSynchronize(s));
+  static MultiArgs m;
+  memset(&m, 0, sizeof m);
+  m.n = n;
+  m.nper = ctxs[0]->n_sms / n;
+  int any = 0;
+  for (int r = 0; r < n; ++r) {
+    failed[r] = 0;
+    m.a[r].absent = 1;
+    if (T[r] < 0) continue;  // absent rank (dead)
+    tg_ctx *c = ctxs[r];
+    if ((st = check_sticky(c))) return st;
+    uint32_t fm = 0;
+    if ((st = replay_args(c, x[r], out[r], T[r], &m.a[r], &m.rk[r], &fm))) return st;
+    failed[r] = fm;
+    if (!fm) {
+      m.a[r].absent = 1;
+      continue;
+    }
+    m.a[r].cta0 = r * m.nper;
+    m.a[r].ncta = m.nper;
+    m.a[r].pdl = 0;
+    m.a[r].absent = 0;
+    m.maps[r] = c->maps_dev;
+    any = 1;
+  }
+  if (!any) return TG_OK;
+  CK2(ctxs[0], launch_layer_multi(m, s));
+  CK2(ctxs[0], cudaStreamSynchronize(s));
+  for (int r = 0; r < n; ++r)
+    if (!m.a[r].absent && (st = replay_status(ctxs[r]))) return st;
   return TG_OK;
 }
 
@@ -1048,7 +1168,7 @@ tg_status tg_finalize(tg_ctx *c) {
       if (c->peer_opened[q]) cudaIpcCloseMemHandle(c->peer[q]);
     cudaFree(c->bank_w1); cudaFree(c->bank_w3); cudaFree(c->bank_w2); cudaFree(c->wg);
     cudaFree(c->w1s); cudaFree(c->w3s); cudaFree(c->w2s);
-    cudaFree(c->sym); cudaFree(c->scratch); cudaFree(c->trace);
+    cudaFree(c->sym); cudaFree(c->scratch); cudaFree(c->trace); cudaFree(c->maps_dev);
     if (c->err_host) cudaFreeHost(c->err_host);
     for (auto &e : c->ev) cudaEventDestroy(e);
     if (c->kv_stream) cudaStreamDestroy(c->kv_stream);

@@ -29,7 +29,7 @@ namespace tg {
 
 #define TG_STAMP(i)                                                                     \
   do {                                                                                  \
-    if (a.trace && threadIdx.x == 0 && blockIdx.x == 0)                                 \
+    if (a.trace && threadIdx.x == 0 && VBID == 0)                                 \
       a.trace[a.n_units_max + 148 + (i)] = globaltimer_ns();                            \
   } while (0)
 
@@ -594,7 +594,7 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
   }
   __syncthreads();
   if (grp == 0 && a.trace && threadIdx.x == 0)
-    a.trace[a.n_units_max + 148 + 40 + (blockIdx.x % nkp)] = globaltimer_ns();  // arrival of each part
+    a.trace[a.n_units_max + 148 + 40 + (VBID % nkp)] = globaltimer_ns();  // arrival of each part
   if (!s_last) return;
   if (grp == 0) TG_STAMP_ANY(30);
   group_topk(a, rk, grp, sm);
@@ -688,13 +688,13 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   // counter is reset here for the next call (the previous call has completed: PDL wait
   // at kernel entry)
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
-  if (blockIdx.x == 0 && threadIdx.x == 0)
+  if (VBID == 0 && threadIdx.x == 0)
     *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
   int nbar = 0;
   TG_STAMP(0);
   // ---- P1 router (+ reset of the GEMM counters of this call)
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
+  for (int i = VBID * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += VGRID * blockDim.x) a.ctr[i] = 0;
+  if (VBID == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
   TG_STAMP(8);
   const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
   {
@@ -706,8 +706,8 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     R.xt = reinterpret_cast<uint32_t *>(fsm + router_wg_bytes(a.d, a.E_r));
     R.red = reinterpret_cast<double *>(fsm + router_wg_bytes(a.d, a.E_r) + R.nbuf * router_xtile_bytes(a.d, a.E_r));
     R.tail = reinterpret_cast<uint8_t *>(R.red);
-    const int bpp = gridDim.x / nkp;  // blocks per K part
-    const int kp = blockIdx.x % nkp, slot = blockIdx.x / nkp;
+    const int bpp = VGRID / nkp;  // blocks per K part
+    const int kp = VBID % nkp, slot = VBID / nkp;
     // Block (kp, slot) runs items (group slot + i * bpp, part kp); its items stream through a
     // cp.async ring of nbuf x tiles (the loads of the next items in flight during this one).
     // Decode-sized calls (one item per block): no grid barrier until the receive layout — the
@@ -741,17 +741,17 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     // every CTA issues its share of the L2 prefetch, behind the router's own loads: the router
     // CTAs after their items (and their top-k chains), the idle ones after a short delay
     if (!(slot < bpp && slot < ngroups)) __nanosleep(2000);
-    l2_prefetch_share(a, blockIdx.x, gridDim.x);
+    l2_prefetch_share(a, VBID, VGRID);
     if (!chain) {
       const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
-      grid_barrier_z(gbar, nbar++, a.err);
-      for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) group_topk(a, rk, grp, reinterpret_cast<float *>(R.tail));
+      grid_barrier_z(gbar, nbar++, a.err, a.ncta);
+      for (int grp = VBID; grp < ngroups; grp += VGRID) group_topk(a, rk, grp, reinterpret_cast<float *>(R.tail));
       TG_STAMP(12);
-      grid_barrier_z(gbar, nbar++, a.err);
-      for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, R.tail);
+      grid_barrier_z(gbar, nbar++, a.err, a.ncta);
+      for (int ch = VBID; ch < nchunks; ch += VGRID) rank_chunk(a, ch, R.tail);
       TG_STAMP(13);
-      grid_barrier_z(gbar, nbar++, a.err);
-      if (blockIdx.x == 0) {
+      grid_barrier_z(gbar, nbar++, a.err, a.ncta);
+      if (VBID == 0) {
         TG_STAMP(1);
         exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(R.tail));
         TG_STAMP(14);
@@ -760,17 +760,17 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
           local_layout(a, threadIdx.x, blockDim.x);
         }
       }
-    } else if (ngroups == 0 && blockIdx.x == 0) {
+    } else if (ngroups == 0 && VBID == 0) {
       // no tokens: the count exchange still runs (peers wait for this rank's counts)
       exchange_counts(a, 0, reinterpret_cast<int32_t *>(R.tail));
     }
   }
-  if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + blockIdx.x] = globaltimer_ns();
-  grid_barrier_z(gbar, nbar++, a.err);
+  if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + VBID] = globaltimer_ns();
+  grid_barrier_z(gbar, nbar++, a.err, a.ncta);
   TG_STAMP(3);
   if (a.local_rows && a.T * a.k > kLocalLayoutBlock) {  // (smaller calls: by the exchange block)
-    local_layout(a, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
-    grid_barrier_z(gbar, nbar++, a.err);
+    local_layout(a, VBID * blockDim.x + threadIdx.x, VGRID * blockDim.x);
+    grid_barrier_z(gbar, nbar++, a.err, a.ncta);
   }
 }
 
@@ -785,13 +785,13 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
 // requests are prioritized").
 __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys &rk, uint8_t *fsm) {
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
-  if (blockIdx.x == 0 && threadIdx.x == 0)
+  if (VBID == 0 && threadIdx.x == 0)
     *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += gridDim.x * blockDim.x) a.ctr[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
+  for (int i = VBID * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += VGRID * blockDim.x) a.ctr[i] = 0;
+  if (VBID == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
   int nbar = 0;
   const int npairs = a.T * a.k;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
+  for (int p = VBID * blockDim.x + threadIdx.x; p < npairs; p += VGRID * blockDim.x) {
     const int K = __ldcg(a.key_old + p);
     int nk = -1;
     if (K >= 0 && ((a.failed >> (K / a.S_max)) & 1u)) {
@@ -800,12 +800,12 @@ __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys 
     }
     a.key[p] = nk;
   }
-  grid_barrier_z(gbar, nbar++, a.err);
+  grid_barrier_z(gbar, nbar++, a.err, a.ncta);
   const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
-  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) rank_chunk(a, ch, fsm);
-  grid_barrier_z(gbar, nbar++, a.err);
-  if (blockIdx.x == 0) exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(fsm));
-  grid_barrier_z(gbar, nbar++, a.err);
+  for (int ch = VBID; ch < nchunks; ch += VGRID) rank_chunk(a, ch, fsm);
+  grid_barrier_z(gbar, nbar++, a.err, a.ncta);
+  if (VBID == 0) exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(fsm));
+  grid_barrier_z(gbar, nbar++, a.err, a.ncta);
 }
 
 // P4 dispatch on `nw` warps (this one is warp `w`, grid-wide numbering): one warp
@@ -908,7 +908,7 @@ __device__ __forceinline__ void dedup_copies(const CallArgs &a, int w, int nw, i
 __device__ __forceinline__ void dispatch_done(const CallArgs &a) {
   const bool sys = a.world > 1;
   fence_scope(sys);
-  if (atomicAdd(&a.sync[3], 1) != (int)gridDim.x - 1) return;
+  if (atomicAdd(&a.sync[3], 1) != (int)VGRID - 1) return;
   fence_scope(sys);
   const uint32_t part = (uint32_t)__ldcg(a.sync + 6);
   for (int q = 0; q < a.world; ++q) {

@@ -204,7 +204,7 @@ __device__ void build_plan(const CallArgs &a, GemmShared *P) {
     P->G1 = bu1;
     P->total = bu1 + bu2;
     P->ngroups = bg;
-    if (blockIdx.x == 0) *a.n_units = bu1 + bu2;
+    if (VBID == 0) *a.n_units = bu1 + bu2;
     if (bg + bred > a.n_ctr_max) {  // capacity guard (sized at init for the worst case)
       atomicExch(a.err, 0x4003);
       P->total = 0;
@@ -275,11 +275,11 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
   return U;
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 1)
-    k_layer(const __grid_constant__ TmaMaps maps, const __grid_constant__ CallArgs a,
-            const __grid_constant__ RouteKeys rk) {
+// The whole layer call for one rank; `maps` are the kernel parameter (k_layer) or a device
+// copy (k_layer_multi: several virtual ranks of one GPU in one cooperative launch).
+__device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &a, const RouteKeys &rk) {
   extern __shared__ uint8_t smem_raw[];
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {  // launch gap: previous call's end -> this entry
+  if (a.trace && VBID == 0 && threadIdx.x == 0) {  // launch gap: previous call's end -> this entry
     a.trace[a.n_units_max + 148 + 19] = a.trace[a.n_units_max + 148 + 17];
     a.trace[a.n_units_max + 148 + 18] = globaltimer_ns();
   }
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // ===================== P4 dispatch (all warps; r01 A/B: 3.5% faster at 4 GPUs than on
   // warps 2-7 beside the first weight loads, equal at 1 GPU) =====================
   if (!a.local_rows) {
-    dispatch_rows(a, blockIdx.x * 8 + (threadIdx.x >> 5), gridDim.x * 8);
+    dispatch_rows(a, VBID * 8 + (threadIdx.x >> 5), VGRID * 8);
     __syncthreads();
     if (threadIdx.x == 0) dispatch_done(a);
   }
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int i = 0; i < 2; ++i) { mbar_init(&S->tfull[i], 1); mbar_init(&S->tempty[i], 128); }
     for (int i = 0; i < kSchedDepth; ++i) { mbar_init(&S->sfull[i], 1); mbar_init(&S->sempty[i], 5); }
     fence_barrier_init();
-    if (a.trace) a.trace[a.n_units_max + blockIdx.x] = globaltimer_ns();
+    if (a.trace) a.trace[a.n_units_max + VBID] = globaltimer_ns();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&maps.w1);
@@ -367,9 +367,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (dedup) {  // and the rows the dedup copies fill in (all CTAs, sync[4])
             const int *dd = a.sync + 4;
-            if (ld_acquire_gpu(dd) < (int)gridDim.x) {
+            if (ld_acquire_gpu(dd) < (int)VGRID) {
               const uint64_t t0 = globaltimer_ns();
-              while (ld_acquire_gpu(dd) < (int)gridDim.x)
+              while (ld_acquire_gpu(dd) < (int)VGRID)
                 if (globaltimer_ns() - t0 > kWaitTimeoutNs) device_fail(err, 0x4004);
             }
           }
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     if (a.local_rows && (warp == 2 || warp == 3)) {
       // ===================== P4 at world == 1: rows copied in receive-row order (warps 2-3) =====================
-      dispatch_local_rows(a, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, S->nrecv, [&](int r, bool shr) {
+      dispatch_local_rows(a, VBID * 2 + (warp - 2), VGRID * 2, S->nrecv, [&](int r, bool shr) {
         if (shr) return S->goff[a.S_loc] + r / a.bn;
         const int s = find_seg(S->rowoff, a.S_loc, r);
         return S->goff[s] + (r - S->rowoff[s]) / a.bn;
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       __syncwarp();
-      dedup_copies(a, blockIdx.x * 6 + (warp - 2), gridDim.x * 6, S->nrecv);
+      dedup_copies(a, VBID * 6 + (warp - 2), VGRID * 6, S->nrecv);
       named_bar_sync(2, 192);
       if (threadIdx.x == 64) {
         __threadfence();
@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // arrivals count 128-column output tiles (a dual unit stores two; d % 256 == 0 when dual)
     const int target = (a.k + (a.Fsh > 0 ? 1 : 0)) * ((a.d + BM - 1) / BM);
     const bf16 *ybuf = reinterpret_cast<const bf16 *>(a.sym[a.rank] + a.L.ybuf);
-    for (int t = blockIdx.x * 8 + warp; t < a.T; t += gridDim.x * 8) {
+    for (int t = VBID * 8 + warp; t < a.T; t += VGRID * 8) {
       if (lane == 0) wait_ctr_ge(a.tokctr + t, target, err, 0x5002);
       __syncwarp();
       __threadfence();
@@ -767,15 +767,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     return;
   }
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 10);
-  grid_barrier(gbar, a.epoch, 1, 0, err);
+  grid_barrier(gbar, a.epoch, 1, 0, err, a.ncta);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 16] = globaltimer_ns();
+  if (a.trace && VBID == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 16] = globaltimer_ns();
   // combine flags: every rank taking part in this run waits for every other one (not only the
   // EWs it sent rows to), so all survivors see a rank that fails mid-run in the same run and
   // take part in the failover replay together; a peer silent past the failure timeout is
   // recorded as failed (no trap), its pairs are re-routed by tg_failover (§5.1)
   const uint32_t part = (uint32_t)__ldcg(a.sync + 6);
-  if (blockIdx.x == 0 && threadIdx.x < a.world && ((part >> threadIdx.x) & 1u)) {
+  if (VBID == 0 && threadIdx.x < a.world && ((part >> threadIdx.x) & 1u)) {
     // every expert output this rank computed is in its source's combine buffer
     fence_scope(sys);
     uint32_t *fl = reinterpret_cast<uint32_t *>(a.sym[threadIdx.x] + a.L.flags) + a.fslot_comb * kMaxWorld + a.rank;
@@ -790,8 +790,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nch = a.d >> 3;
   const size_t total = (size_t)a.T * nch;
   const bf16 *ybuf = reinterpret_cast<const bf16 *>(a.sym[a.rank] + a.L.ybuf);
-  const size_t nthr = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += 4 * nthr) {
+  const size_t nthr = (size_t)VGRID * blockDim.x;
+  for (size_t i = (size_t)VBID * blockDim.x + threadIdx.x; i < total; i += 4 * nthr) {
     // four chunks (i, i + nthr, ...) per step, of up to four tokens
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -799,7 +799,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (ii < total) combine_chunks<1>(a, ybuf, (int)(ii / nch), (int)(ii % nch), 0);
     }
   }
-  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) a.trace[a.n_units_max + 148 + 17] = globaltimer_ns();
+  if (a.trace && threadIdx.x == 0 && VBID == 0) a.trace[a.n_units_max + 148 + 17] = globaltimer_ns();
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_layer(const __grid_constant__ TmaMaps maps, const __grid_constant__ CallArgs a,
+            const __grid_constant__ RouteKeys rk) {
+  layer_body(maps, a, rk);
+}
+
+// Virtual ranks of one GPU as ONE cooperative launch (tests; a GPU shared by several AW/EW
+// shards): CTA b is CTA b - r * nper of rank r = b / nper.  The ranks wait on one another's
+// flags, so they must be co-resident — separate launches carry no such guarantee.
+__global__ void __launch_bounds__(kGemmThreads, 1) k_layer_multi(const __grid_constant__ MultiArgs m) {
+  const int r = blockIdx.x / m.nper;
+  if (r >= m.n || m.a[r].absent) return;  // a rank that does not take part (died before the call)
+  layer_body(*m.maps[r], m.a[r], m.rk[r]);
 }
 
 size_t gemm_smem_bytes() { return 1024 + (size_t)kRingBytes + sizeof(GemmShared); }
@@ -808,17 +823,16 @@ static constexpr int kLayerSmemMax = 225 * 1024;  // + ~1 KB static smem: under 
 static_assert(1024 + kRingBytes + sizeof(GemmShared) <= kLayerSmemMax, "GEMM smem over budget");
 
 cudaError_t layer_configure() {
-  return cudaFuncSetAttribute(k_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, kLayerSmemMax);
+  cudaError_t e = cudaFuncSetAttribute(k_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, kLayerSmemMax);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_layer_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, kLayerSmemMax);
 }
 
 size_t layer_smem_bytes(const CallArgs &a) { return tg_max(gemm_smem_bytes(), front_smem(a)); }
 
-// n_ctas: one CTA per SM (cooperative launch: the grid barriers need every CTA resident), or
-// fewer when several virtual ranks share the GPU (tests: each rank's grid is a share of the
-// SMs, all resident at once; no cooperative attribute and no programmatic dependent launch,
-// whose early-resident CTAs could hold SMs another rank's grid is waiting for).
-cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_ctas, bool shared_gpu,
-                         cudaStream_t s) {
+// One CTA per SM, cooperative (the grid barriers need every CTA resident); programmatic
+// dependent launch lets the next call's launch overlap this call's end.
+cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_ctas, cudaStream_t s) {
   if (layer_smem_bytes(a) > (size_t)kLayerSmemMax) return cudaErrorInvalidConfiguration;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_ctas);
@@ -831,8 +845,25 @@ cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = shared_gpu ? 0 : (a.pdl ? 2 : 1);
+  cfg.numAttrs = a.pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k_layer, maps, a, rk);
+}
+
+cudaError_t launch_layer_multi(const MultiArgs &m, cudaStream_t s) {
+  size_t smem = 0;
+  for (int r = 0; r < m.n; ++r) smem = tg_max(smem, layer_smem_bytes(m.a[r]));
+  if (smem > (size_t)kLayerSmemMax) return cudaErrorInvalidConfiguration;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(m.n * m.nper);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_layer_multi, m);
 }
 
 }  // namespace tg

@@ -144,6 +144,9 @@ struct CallArgs {
   int local_rows;        // world == 1: rows copied in row order beside the GEMM, per-tile counters
   int local_comb;        // world == 1: per-token arrival counters, combine without a grid barrier
   int dev;               // development A/B switches (TG_DEV)
+  int cta0, ncta;        // this rank's CTAs in the launch: [cta0, cta0 + ncta) (several virtual ranks
+                         // of one GPU share one cooperative launch: tg_moe_layer_multi)
+  int absent;            // virtual rank that does not take part in this launch (its CTAs exit)
   int32_t *n_units;      // [1] units of the last call (written by the GEMM, diagnostics)
   int n_units_max;       // capacity bound (trace sizing)
   int *err;              // host-mapped error word
@@ -159,11 +162,24 @@ struct CallArgs {
   SymLayout L;
 };
 
+// A CTA's block index and the CTA count within its rank's grid (every device function that
+// distributes work over the grid takes them from its CallArgs `a`).
+#define VBID ((int)blockIdx.x - a.cta0)
+#define VGRID (a.ncta)
+
+constexpr int kMaxVirt = 4;  // virtual ranks per fused launch
+struct MultiArgs {           // one cooperative launch over the virtual ranks of one GPU
+  CallArgs a[kMaxVirt];
+  RouteKeys rk[kMaxVirt];
+  const TmaMaps *maps[kMaxVirt];  // device copies (TMA descriptors in global memory)
+  int n, nper;                    // ranks, CTAs per rank
+};
+
 // Kernel launchers (tg_export.cu / tg_gemm.cu).  Return cudaGetLastError().
 // the whole layer call: one cooperative launch of k_layer (front P1-P3, then
 // dispatch || grouped GEMM, combine)
-cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_ctas, bool shared_gpu,
-                         cudaStream_t s);
+cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &maps, int n_ctas, cudaStream_t s);
+cudaError_t launch_layer_multi(const MultiArgs &m, cudaStream_t s);
 cudaError_t launch_export_keys(const CallArgs &a, int n, int32_t *dst_rank, int32_t *dst_slot, cudaStream_t s);
 cudaError_t layer_configure();
 size_t gemm_smem_bytes();

@@ -230,17 +230,18 @@ __device__ __forceinline__ void wait_ctr_ge(const int *ctr, int target, int *err
 
 // Grid-wide barrier for a cooperative launch (all CTAs co-resident).  `count`
 // is a 64-bit counter that is never reset: barrier i of call `epoch` (1-based)
-// completes when count reaches ((epoch-1)*nbar + i+1) * gridDim.x.
+// completes when count reaches ((epoch-1)*nbar + i+1) * nct (nct = CTAs of the rank's grid).
 __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long *p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void grid_barrier(unsigned long long *count, uint32_t epoch, int nbar, int i, int *err) {
+__device__ __forceinline__ void grid_barrier(unsigned long long *count, uint32_t epoch, int nbar, int i, int *err,
+                                             unsigned nct) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned long long target =
-        ((unsigned long long)(epoch - 1) * nbar + (unsigned long long)(i + 1)) * gridDim.x;
+        ((unsigned long long)(epoch - 1) * nbar + (unsigned long long)(i + 1)) * nct;
     __threadfence();
     atomicAdd(count, 1ull);
     if (ld_acquire_gpu_u64(count) < target) {
@@ -254,11 +255,11 @@ __device__ __forceinline__ void grid_barrier(unsigned long long *count, uint32_t
 }
 
 // Grid barrier on a counter that starts at 0 for this call (barrier i completes
-// at (i + 1) * gridDim.x arrivals): the number of barriers may vary per call.
-__device__ __forceinline__ void grid_barrier_z(unsigned long long *count, int i, int *err) {
+// at (i + 1) * nct arrivals): the number of barriers may vary per call.
+__device__ __forceinline__ void grid_barrier_z(unsigned long long *count, int i, int *err, unsigned nct) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned long long target = (unsigned long long)(i + 1) * gridDim.x;
+    const unsigned long long target = (unsigned long long)(i + 1) * nct;
     __threadfence();
     atomicAdd(count, 1ull);
     if (ld_acquire_gpu_u64(count) < target) {

@@ -176,13 +176,14 @@ def test_load_experts_guards_active_table_slots():
 def test_virtual_rank_and_stage_calls_host_only():
     """Host-only ctxs refuse the device-side bootstrap / export entry points."""
     tg, ctx, pl = _host_ctx()
-    for fn, args in ((tg.tg_set_launch_ctas, (4,)), (tg.tg_set_stage_export, (1,)),
-                     (tg.tg_connect_local, ([ctx],))):
+    for fn, args in ((tg.tg_set_stage_export, (1,)), (tg.tg_connect_local, ([ctx],))):
         with pytest.raises(tg.TarragonError) as ei:
             fn(ctx, *args)
         assert ei.value.status == tg.TG_ERR_UNSUPPORTED
     with pytest.raises(tg.TarragonError):
         tg.tg_get_stage(ctx, tg.TG_STAGE_Y)
+    # fused virtual-rank launches need device ctxs of ranks 0..world-1 on one device
+    assert tg.tg_moe_layer_multi([ctx], [None], [None]) == tg.TG_ERR_INVALID
     tg.tg_finalize(ctx)
 
 

@@ -1,12 +1,11 @@
 """The multi-rank data plane on ONE GPU: G virtual ranks (one ctx each, same process, same
-device) connected by device pointer (tg_connect_local) and launched on n_SM / G CTAs each, on
-their own streams.  Count exchange, peer dispatch stores, the combine exchange fused into the
+device) connected by device pointer (tg_connect_local), their calls run as ONE cooperative
+launch (tg_moe_layer_multi: rank r on CTAs [r n_SM / G, (r + 1) n_SM / G)).  Count exchange, peer dispatch stores, the combine exchange fused into the
 GEMM2 epilogue, epoch flags, token dedup, masks, rank fail-stop and in-call failover run the
 same code as over NVLink (peer addresses are just other ranks' regions); only the transport
 differs.  SURVEY.md 8(e), P:739 (no collective group per call), P:914-920 (in-call failover),
 P:927-941 (EWs tolerate AW failures)."""
 import os
-import threading
 
 import numpy as np
 import pytest
@@ -45,28 +44,19 @@ class World:
             if fail_ms:
                 tg.tg_set_failure_timeout(l.ctx, fail_ms)
         self.xs = [self.x[r * self.Tr:(r + 1) * self.Tr].contiguous().cuda() for r in range(G)]
-        self.streams = [torch.cuda.Stream() for _ in range(G)]
 
     def call(self, skip=(), xs=None):
-        rcs, outs, _ = self.tg.call_all(self.layers, xs or self.xs, streams=self.streams, skip=skip)
+        rc, outs = self.tg.call_all(self.layers, xs or self.xs, skip=skip)
         torch.cuda.synchronize()
-        for r, rc in enumerate(rcs):
-            assert rc in (None, self.tg.TG_OK), f"rank {r}: {self.tg.STATUS.get(rc, rc)}"
+        assert rc == self.tg.TG_OK, self.tg.tg_last_error(self.layers[0].ctx)
         return outs
 
     def failover_all(self, outs, ranks):
-        """tg_failover is collective among the survivors: one host thread per virtual rank."""
-        res = {}
-
-        def go(r):
-            res[r] = self.layers[r].failover(self.xs[r], outs[r], self.streams[r])
-        th = [threading.Thread(target=go, args=(r,)) for r in ranks]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
+        """tg_failover of every survivor (collective among them): one fused replay launch."""
+        skip = [r for r in range(self.G) if r not in ranks]
+        rc, failed = self.tg.failover_all(self.layers, self.xs, outs, skip=skip)
         torch.cuda.synchronize()
-        return res
+        return {r: (rc, failed[r]) for r in ranks}
 
     def check(self, outs, mask=None, tokens=None):
         views = [collect(l, o, t0=r * self.Tr) for r, (l, o) in enumerate(zip(self.layers, outs))]
