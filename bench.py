@@ -320,9 +320,13 @@ def failover_record(tg, layer, shape, xs, stream, N, rank, dev, n_calls=40):
     rc = tg.tg_mask_worker(layer.ctx, 1, 1)
     t_mask = time.perf_counter() - t0
     outs_post = [torch.empty_like(xs[0]) for _ in xs]
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
     rc2 = tg.tg_moe_layer(layer.ctx, xs[0], outs_post[0], stream)
+    r1.record(stream)
     torch.cuda.synchronize()
     t_reroute = time.perf_counter() - t0
+    first_ms = r0.elapsed_time(r1)
     # fail-stop semantics: nothing may read the masked EW's memory any more
     if pl.ew_rank[1] == rank:
         nan = torch.full((shape.F, shape.d), float("nan"), dtype=torch.bfloat16, device=dev)
@@ -336,7 +340,9 @@ def failover_record(tg, layer, shape, xs, stream, N, rank, dev, n_calls=40):
     ident = sum(int(torch.equal(a.view(torch.int16), b.view(torch.int16))) for a, b in zip(ref, outs_post))
     errors = int(rc not in (tg.TG_OK,)) + int(rc2 != tg.TG_OK)
     return {"protocol": "SURVEY 8(d): mask EW1 on every rank mid-stream, NaN-poison its slots",
-            "ews": pl.n_ews, "ranks": N, "mask_host_us": t_mask * 1e6, "reroute_ms": t_reroute * 1e3,
+            "ews": pl.n_ews, "ranks": N, "mask_host_us": t_mask * 1e6,
+            "reroute_ms": t_mask * 1e3 + first_ms, "first_post_mask_call_us": first_ms * 1e3,
+            "reroute_host_wall_ms": t_reroute * 1e3,
             "pre_us_per_call": float(np.median(pre)) * 1e3, "post_us_per_call": float(np.median(post)) * 1e3,
             "calls_errored": errors, "post_mask_outputs_bit_identical": ident, "post_mask_outputs_compared": len(ref),
             "paper_context": "EW-failure stall ~0.3 s on H200 + RDMA (P:1257), not comparable hardware"}

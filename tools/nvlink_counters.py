@@ -30,22 +30,46 @@ import paper_2601_01310_b200 as tg  # noqa: E402
 from bench import make_weights_device  # noqa: E402
 
 
-def nvlink_kib(handle, nlinks=18):
+NVML_RC = {}
+
+
+def smi_kib(index):
+    """Fallback: `nvidia-smi nvlink -gt d` data throughput counters (KiB, summed over the links)."""
+    import re
+    import subprocess
+    r = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(index)], capture_output=True, text=True)
+    tx = sum(int(v) for v in re.findall(r"Data Tx:\s*(\d+)\s*KiB", r.stdout))
+    rx = sum(int(v) for v in re.findall(r"Data Rx:\s*(\d+)\s*KiB", r.stdout))
+    NVML_RC["smi_tail"] = r.stdout[-300:] + r.stderr[-200:]
+    return tx, rx
+
+
+def nvlink_kib(handle, index, nlinks=18):
     import pynvml as p
     ids = []
     for f in (p.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, p.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX):
         for l in range(nlinks):
             ids.append((f, l))
-    vals = p.nvmlDeviceGetFieldValues(handle, ids)
     tx = rx = 0
-    for (f, _), v in zip(ids, vals):
-        if v.nvmlReturn != 0:
-            continue
-        x = v.value.ullVal
-        if f == p.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX:
-            tx += x
-        else:
-            rx += x
+    ok = False
+    try:
+        vals = p.nvmlDeviceGetFieldValues(handle, ids)
+        for (f, _), v in zip(ids, vals):
+            NVML_RC[v.nvmlReturn] = NVML_RC.get(v.nvmlReturn, 0) + 1
+            if v.nvmlReturn != 0:
+                continue
+            ok = True
+            x = v.value.ullVal
+            if f == p.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX:
+                tx += x
+            else:
+                rx += x
+    except Exception as e:  # noqa: BLE001
+        NVML_RC["exc"] = str(e)
+    if not ok or (tx == 0 and rx == 0):
+        NVML_RC["source"] = "nvidia-smi"
+        return smi_kib(index)
+    NVML_RC["source"] = "nvml"
     return tx, rx
 
 
@@ -77,14 +101,14 @@ def main():
         layer(x, out)
     torch.cuda.synchronize()
     dist.barrier()
-    tx0, rx0 = nvlink_kib(h)
+    tx0, rx0 = nvlink_kib(h, local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(a.calls):
         layer(x, out)
     e1.record()
     torch.cuda.synchronize()
-    tx1, rx1 = nvlink_kib(h)
+    tx1, rx1 = nvlink_kib(h, local)
     dist.barrier()
     ms = e0.elapsed_time(e1) / a.calls
     # algorithmic exchange bytes of this rank (per call): dispatched rows to peers + y rows stored in peers
@@ -107,9 +131,12 @@ def main():
            "nvlink_rx_MB_per_call": (rx1 - rx0) * 1024 / a.calls / 1e6,
            "pairs_to_peers": to_peers, "rows_from_peers": int(counts[rank].sum()) - int((dr == rank).sum()),
            "algorithmic_dispatch_MB": to_peers * sh.d * 2 / 1e6,
-           "dispatch_phase_us": disp_us, "combine_phase_us": comb_us}
+           "dispatch_phase_us": disp_us, "combine_phase_us": comb_us,
+           "counter_source": {str(k): v for k, v in NVML_RC.items()}}
     if disp_us:
         rec["dispatch_GBps_per_direction"] = rec["algorithmic_dispatch_MB"] * 1e6 / (disp_us * 1e-6) / 1e9
+    if rec["nvlink_tx_MB_per_call"] > 0 and disp_us and comb_us:
+        rec["counter_GBps_tx_over_exchange_phases"] = rec["nvlink_tx_MB_per_call"] * 1e6 / ((disp_us + comb_us) * 1e-6) / 1e9
     recs = [None] * world
     dist.all_gather_object(recs, rec)
     if rank == 0:
