@@ -106,6 +106,8 @@ struct tg_ctx {
   struct KvRec { tg_ctx *c; uint64_t seq; } kv_rec[kKvRecs];
   int kv_next = 0;
   int last_T = 0;
+  float *w_buf[2] = {nullptr, nullptr}, *sg_buf[2] = {nullptr, nullptr};  // by call parity
+  int last_wb = 0;                                                        // parity of the last call
   int last_launches = 0;
   bool sticky = false;
   // profiling
@@ -298,13 +300,15 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   auto carve = [&](size_t bytes) { size_t o = so; so = align_up(so + bytes, 256); return o; };
   size_t o_sg = carve(Tm * 4);
   size_t o_lg = carve(Tm * (size_t)(E + 1) * 4);
-  size_t o_idx = carve(Tm * k * 4), o_w = carve(Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
+  size_t o_idx = carve(Tm * k * 4), o_w = carve(2 * Tm * k * 4), o_key = carve(Tm * k * 4), o_lrank = carve(Tm * k * 4);
+  size_t o_sgb = carve(2 * Tm * 4);
   size_t o_key2 = carve(Tm * k * 4);
   size_t o_lp = carve(((Tm + 31) / 32) * (size_t)(d / 64) * 32 * (E + 1) * 4);  // groups * nkp * 32 * E floats (KP >= 64)
-  size_t o_gc2 = carve(((Tm + 31) / 32) * 4), o_cc = carve((size_t)(1 + nblk_max) * 4);
+  const int gmax = (int)((Tm + 31) / 32), cmax = 1 + nblk_max;
+  size_t o_gc2 = carve(3 * (size_t)gmax * 4), o_cc = carve(3 * (size_t)cmax * 4);
   size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
   size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
-  size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(64);
+  size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(128);
   const int n_grp_max = nt_max + nt_sh + 16;
   c->args.n_ctr_all = c->args.n_ctr_max + n_grp_max + (int)Tm;
   size_t o_ctr = carve((size_t)c->args.n_ctr_all * 4);
@@ -332,6 +336,13 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
     a.l2_prefetch_bytes = e ? atoll(e) : (long long)(prop.l2CacheSize * 0.6);
   }
   a.idx = (int32_t *)(sb + o_idx); a.w = (float *)(sb + o_w); a.sgate = (float *)(sb + o_sg);
+  // gate weights and shared-gate values: one buffer per call parity (the next call's front writes
+  // them while this call's combine may still read its own, under PDL)
+  for (int i = 0; i < 2; ++i) {
+    c->w_buf[i] = (float *)(sb + o_w) + (size_t)i * Tm * k;
+    c->sg_buf[i] = (float *)(sb + o_sgb) + (size_t)i * Tm;
+  }
+  a.gmax = gmax; a.cmax = cmax;
   c->logits = (float *)(sb + o_lg);
   a.gate_mode = c->gate_mode; a.shared_gate = c->shared_gate; a.E_r = E + c->shared_gate; a.key = (int32_t *)(sb + o_key);
   c->key_main = a.key; c->key_replay = (int32_t *)(sb + o_key2);
@@ -638,7 +649,7 @@ tg_status tg_get_stage(tg_ctx *c, int stage, void *dst, size_t cap, size_t *byte
     case TG_STAGE_Y: src = c->sym + c->L.ybuf; n = T * c->k * c->d * 2; break;
     case TG_STAGE_HSH: src = a.Hs; n = c->Fsh ? T * c->Fsh * 2 : 0; break;
     case TG_STAGE_YSH: src = a.ysh; n = c->Fsh ? T * c->d * 2 : 0; break;
-    case TG_STAGE_SGATE: src = a.sgate; n = c->shared_gate ? T * 4 : 0; break;
+    case TG_STAGE_SGATE: src = c->sg_buf[c->last_wb]; n = c->shared_gate ? T * 4 : 0; break;
     default: return fail(c, TG_ERR_INVALID, "unknown stage %d", stage);
   }
   *bytes = n;
@@ -700,6 +711,7 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
   a.cta0 = 0;
   a.ncta = c->n_sms;
   a.absent = 0;
+  a.cbuf = (int)(a.epoch % 3);
   a.replay = 0;
   a.failed = 0;
   a.key_old = nullptr;
@@ -730,6 +742,9 @@ static tg_status prepare_call(tg_ctx *c, const void *x, void *out, int T, CallAr
   a->xepoch = ++c->xepoch;
   a->fepoch = a->xepoch;
   a->cnt_buf = (int)(a->xepoch & 1);
+  c->last_wb = (int)(a->xepoch & 1);
+  a->w = c->w_buf[c->last_wb];
+  a->sgate = c->sg_buf[c->last_wb];
   a->inject_fail = c->inject_next ? 1 : 0;
   c->inject_next = false;
   return TG_OK;
@@ -849,6 +864,8 @@ static tg_status replay_args(tg_ctx *c, const void *x, void *out, int T, CallArg
   a->failed = fm;
   a->key_old = c->key_main;
   a->key = c->key_replay;
+  a->w = c->w_buf[c->last_wb];  // the failed call's gate weights (its combine is redone)
+  a->sgate = c->sg_buf[c->last_wb];
   a->logits = nullptr;
   a->local_rows = 0;  // a replay is a multi-rank run (world > 1)
   a->local_comb = 0;
@@ -1004,7 +1021,7 @@ tg_status tg_get_routing(tg_ctx *c, int n_tokens, int32_t *idx, float *w, int32_
   CK(cudaSetDevice(c->device));
   const size_t n = (size_t)c->last_T * c->k;
   if (idx && n) CK(cudaMemcpyAsync(idx, c->args.idx, n * 4, cudaMemcpyDeviceToDevice, s));
-  if (w && n) CK(cudaMemcpyAsync(w, c->args.w, n * 4, cudaMemcpyDeviceToDevice, s));
+  if (w && n) CK(cudaMemcpyAsync(w, c->w_buf[c->last_wb], n * 4, cudaMemcpyDeviceToDevice, s));
   if (dst_pos && n) CK(cudaMemcpyAsync(dst_pos, c->args.dst_pos, n * 4, cudaMemcpyDeviceToDevice, s));
   if (counts) CK(cudaMemcpyAsync(counts, c->args.gcounts, (size_t)c->nkeys * 4, cudaMemcpyDeviceToDevice, s));
   if ((dst_rank || dst_slot) && n) CK(launch_export_keys(c->args, (int)n, dst_rank, dst_slot, s));

@@ -585,16 +585,12 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
   __shared__ int s_last;
   if (threadIdx.x == 0) {
     __threadfence();
-    const int last = atomicAdd(a.grp_ctr + grp, 1) == nkp - 1;
-    if (last) {
-      a.grp_ctr[grp] = 0;
-      __threadfence();
-    }
+    const int last = atomicAdd(a.grp_ctr + (size_t)a.cbuf * a.gmax + grp, 1) == nkp - 1;
     s_last = last;
   }
   __syncthreads();
   if (grp == 0 && a.trace && threadIdx.x == 0)
-    a.trace[a.n_units_max + 148 + 40 + (VBID % nkp)] = globaltimer_ns();  // arrival of each part
+    a.trace[a.n_units_max + 148 + 40 + (grp % nkp)] = globaltimer_ns();  // arrival (group 0: slot of part)
   if (!s_last) return;
   if (grp == 0) TG_STAMP_ANY(30);
   group_topk(a, rk, grp, sm);
@@ -604,11 +600,7 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
   const int ng_ch = min(gpc, ngroups - ch * gpc);
   if (threadIdx.x == 0) {
     __threadfence();
-    const int last = atomicAdd(a.chunk_ctr + 1 + ch, 1) == ng_ch - 1;
-    if (last) {
-      a.chunk_ctr[1 + ch] = 0;
-      __threadfence();
-    }
+    const int last = atomicAdd(a.chunk_ctr + (size_t)a.cbuf * a.cmax + 1 + ch, 1) == ng_ch - 1;
     s_last = last;
   }
   __syncthreads();
@@ -617,15 +609,12 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
   if (ch == 0) TG_STAMP_ANY(13);
   if (threadIdx.x == 0) {
     __threadfence();
-    const int last = atomicAdd(a.chunk_ctr, 1) == nchunks - 1;
-    if (last) {
-      a.chunk_ctr[0] = 0;
-      __threadfence();
-    }
+    const int last = atomicAdd(a.chunk_ctr + (size_t)a.cbuf * a.cmax, 1) == nchunks - 1;
     s_last = last;
   }
   __syncthreads();
   if (!s_last) return;
+  griddep_wait();  // the exchange and everything after it touch state the previous call may use
   TG_STAMP_ANY(1);
   exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(sm));
   TG_STAMP_ANY(14);
@@ -680,6 +669,26 @@ __device__ void l2_prefetch_share(const CallArgs &a, int part, int nparts) {
   }
 }
 
+// Programmatic dependent launch: the previous call triggers its dependents when its GEMM phase
+// starts, so this call's CTAs start (on the SMs its tail frees) before it has completed.  Until
+// griddepcontrol.wait a CTA touches only this call's input x, the router / top-k / rank scratch
+// (the previous call is past its front) and state kept per call parity (gate weights) or per
+// launch mod 3 (arrival counters: reset two launches ahead, below).
+
+// After griddepcontrol.wait (the previous launch has completed): reset what this launch's GEMM
+// phase counts on, and the counter set of the launch after next.
+__device__ __forceinline__ void post_wait_resets(const CallArgs &a) {
+  for (int i = VBID * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += VGRID * blockDim.x) a.ctr[i] = 0;
+  const int nb = (a.cbuf + 2) % 3;
+  for (int i = VBID * blockDim.x + threadIdx.x; i < a.gmax; i += VGRID * blockDim.x) a.grp_ctr[(size_t)nb * a.gmax + i] = 0;
+  for (int i = VBID * blockDim.x + threadIdx.x; i < a.cmax; i += VGRID * blockDim.x) a.chunk_ctr[(size_t)nb * a.cmax + i] = 0;
+  if (VBID == 0 && threadIdx.x == 0) {
+    *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
+    a.sync[16 + nb] = 0;
+  }
+  if (VBID == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
+}
+
 // P1..P3 (all 256 threads of every CTA; cooperative grid).  Ends with a grid
 // barrier: the receive layout (dbase, slot_rows, need_src, ...) is then visible
 // to every CTA.  fsm: this CTA's dynamic shared memory (front layout).
@@ -688,13 +697,14 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   // counter is reset here for the next call (the previous call has completed: PDL wait
   // at kernel entry)
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
-  if (VBID == 0 && threadIdx.x == 0)
-    *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
   int nbar = 0;
   TG_STAMP(0);
-  // ---- P1 router (+ reset of the GEMM counters of this call)
-  for (int i = VBID * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += VGRID * blockDim.x) a.ctr[i] = 0;
-  if (VBID == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
+  // ---- P1 router: router items go to the CTAs in the order they start (under PDL the first
+  // ones start on the SMs the previous call's tail frees)
+  __shared__ int s_item;
+  if (threadIdx.x == 0) s_item = atomicAdd(a.sync + 16 + a.cbuf, 1);
+  __syncthreads();
+  const int bitem = s_item;
   TG_STAMP(8);
   const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
   {
@@ -707,7 +717,7 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     R.red = reinterpret_cast<double *>(fsm + router_wg_bytes(a.d, a.E_r) + R.nbuf * router_xtile_bytes(a.d, a.E_r));
     R.tail = reinterpret_cast<uint8_t *>(R.red);
     const int bpp = VGRID / nkp;  // blocks per K part
-    const int kp = VBID % nkp, slot = VBID / nkp;
+    const int kp = bitem % nkp, slot = bitem / nkp;
     // Block (kp, slot) runs items (group slot + i * bpp, part kp); its items stream through a
     // cp.async ring of nbuf x tiles (the loads of the next items in flight during this one).
     // Decode-sized calls (one item per block): no grid barrier until the receive layout — the
@@ -741,7 +751,9 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     // every CTA issues its share of the L2 prefetch, behind the router's own loads: the router
     // CTAs after their items (and their top-k chains), the idle ones after a short delay
     if (!(slot < bpp && slot < ngroups)) __nanosleep(2000);
-    l2_prefetch_share(a, VBID, VGRID);
+    l2_prefetch_share(a, bitem, VGRID);
+    griddep_wait();
+    post_wait_resets(a);
     if (!chain) {
       const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
       grid_barrier_z(gbar, nbar++, a.err, a.ncta);
@@ -762,6 +774,7 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
       }
     } else if (ngroups == 0 && VBID == 0) {
       // no tokens: the count exchange still runs (peers wait for this rank's counts)
+      __syncthreads();  // this block's share of the resets above
       exchange_counts(a, 0, reinterpret_cast<int32_t *>(R.tail));
     }
   }
@@ -785,10 +798,8 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
 // requests are prioritized").
 __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys &rk, uint8_t *fsm) {
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
-  if (VBID == 0 && threadIdx.x == 0)
-    *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
-  for (int i = VBID * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += VGRID * blockDim.x) a.ctr[i] = 0;
-  if (VBID == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
+  griddep_wait();
+  post_wait_resets(a);
   int nbar = 0;
   const int npairs = a.T * a.k;
   for (int p = VBID * blockDim.x + threadIdx.x; p < npairs; p += VGRID * blockDim.x) {

@@ -283,8 +283,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
     a.trace[a.n_units_max + 148 + 19] = a.trace[a.n_units_max + 148 + 17];
     a.trace[a.n_units_max + 148 + 18] = globaltimer_ns();
   }
-  // PDL: everything below reads/writes state of the previous call's kernel
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // PDL: the front waits (griddepcontrol.wait) before it touches state of the previous call
   // ===================== front: P1 router .. P3 count exchange (tg_front.cuh) =====================
   if (a.replay) replay_front(a, rk, smem_raw);
   else front_phase(a, rk, smem_raw);
@@ -296,6 +295,9 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
     if (threadIdx.x == 0) dispatch_done(a);
   }
   if (a.inject_fail) return;  // fault injection (tests): crash after the dispatch, the peers hold the rows
+  // the next call may start now (PDL): its front runs on the SMs this call's tail frees, and waits
+  // for this call's completion before it touches shared state
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // the ring below is refilled by TMA (async proxy) after the front's generic smem writes
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   // 1024-B aligned stage ring (128-B swizzle atoms), bookkeeping after it.
@@ -754,7 +756,6 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
     // warp per token, grid-stride from this CTA's warps as soon as its GEMM work is done: a
     // token is combined once its arrival count is complete (no grid barrier); a lane owns
     // d / 256 chunks of 8 outputs, all their loads in flight
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // arrivals count 128-column output tiles (a dual unit stores two; d % 256 == 0 when dual)
     const int target = (a.k + (a.Fsh > 0 ? 1 : 0)) * ((a.d + BM - 1) / BM);
     const bf16 *ybuf = reinterpret_cast<const bf16 *>(a.sym[a.rank] + a.L.ybuf);
@@ -768,7 +769,6 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
   }
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 10);
   grid_barrier(gbar, a.epoch, 1, 0, err, a.ncta);
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.trace && VBID == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 16] = globaltimer_ns();
   // combine flags: every rank taking part in this run waits for every other one (not only the
   // EWs it sent rows to), so all survivors see a rank that fails mid-run in the same run and
@@ -846,6 +846,10 @@ cudaError_t launch_layer(const CallArgs &a, const RouteKeys &rk, const TmaMaps &
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = a.pdl ? 2 : 1;
+  if (a.dev & 32) {  // A/B: no cooperative attribute (PDL only)
+    cfg.attrs = at + 1;
+    cfg.numAttrs = a.pdl ? 1 : 0;
+  }
   return cudaLaunchKernelEx(&cfg, k_layer, maps, a, rk);
 }
 

@@ -121,8 +121,11 @@ struct CallArgs {
   int32_t *key;          // [T_max][k] destination key of each pair
   int32_t *lrank;        // [T_max][k] rank of the pair within its block and key
   float *logit_part;     // [ceil(T_max/32)][nkp][32][E] router partial logits
-  int32_t *grp_ctr;      // [ceil(T_max/32)] K-part arrival counters (reset by the last arriver)
-  int32_t *chunk_ctr;    // [1 + ceil(T_max/256)]: [0] chunks ranked, [1 + c] groups of chunk c done
+  int32_t *grp_ctr;      // [3][gmax] K-part arrival counters, set cbuf of this launch
+  int32_t *chunk_ctr;    // [3][cmax]: [0] chunks ranked, [1 + c] groups of chunk c done
+  int gmax, cmax;        // entries per set
+  int cbuf;              // epoch % 3: the counter set of this launch (the set two launches ahead is
+                         // reset after griddepcontrol.wait: launches overlap under PDL)
   int32_t *bcnt;         // [nblk_max][nkeys] per-block counts -> exclusive block bases
   int32_t *dbase;        // [nkeys] base row of this source in each (rank, slot)
   int32_t *dst_pos;      // [T_max][k]
@@ -133,7 +136,7 @@ struct CallArgs {
   int64_t *stats;        // [nkeys]
   int32_t *sync;         // [0..4] counters (scheduler, CTAs done, dispatch blocks, -, dedup copies), [5] dedup on,
                          // [6] ranks taking part in this run (alive and heard from in the count exchange);
-                         // u64 grid barriers at [8], [10], [12]
+                         // u64 grid barriers at [8], [10], [12]; [16 + cbuf] router item counters
   float *logits;         // [T_max][E_r] router logits of the last call (parity export; nullptr = off)
   int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters, then rdy and tokctr
   int n_ctr_max;

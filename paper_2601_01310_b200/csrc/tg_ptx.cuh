@@ -272,6 +272,10 @@ __device__ __forceinline__ void grid_barrier_z(unsigned long long *count, int i,
   __syncthreads();
 }
 
+// Programmatic dependent launch: wait until the previous grid in the stream has completed and its
+// memory is visible (a no-op without the launch attribute).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
