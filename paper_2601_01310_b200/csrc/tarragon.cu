@@ -362,6 +362,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   {
     const char *e = getenv("TG_PDL");  // development switch for A/B timing; default on
     a.pdl = (e && e[0] == '0') ? 0 : 1;
+    const char *co = getenv("TG_COOP");
+    a.coop = (co && co[0] == '1') ? 1 : 0;
     const char *wm = getenv("TG_WIDE");
     if (wm && (wm[0] == '0' || wm[0] == '1')) c->force_mode = wm[0] - '0';
     const char *dm = getenv("TG_G2DUAL");

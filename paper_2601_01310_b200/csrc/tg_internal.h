@@ -154,6 +154,7 @@ struct CallArgs {
   int n_units_max;       // capacity bound (trace sizing)
   int *err;              // host-mapped error word
   int pdl;               // programmatic dependent launch between consecutive calls
+  int coop;              // cooperative launch attribute with PDL (TG_COOP=1; holds PDL's early start back)
   uint64_t *trace;       // optional GEMM trace: [n_units_max] (end_ns << 16 | smid), [gridDim] start_ns
   // GEMM buffers (local)
   bf16 *H;               // [R_cap][F]
