@@ -283,6 +283,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   L.dup = off; off = align_up(off + (size_t)c->R_tot * 4, 1024);
   L.ybuf = off; off = align_up(off + Tm * k * d * 2, 1024);
   L.cnt_all = off; off = align_up(off + (size_t)3 * world * c->nkeys * 4, 1024);
+  L.tokctr = off; off = align_up(off + Tm * 4, 1024);
   L.flags = off; off = align_up(off + kNumFlagKinds * kMaxWorld * 4, 1024);
   L.total = off;
   CKI(cudaMalloc(&c->sym, L.total));
@@ -310,7 +311,7 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
   size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(128);
   const int n_grp_max = nt_max + nt_sh + 16;
-  c->args.n_ctr_all = c->args.n_ctr_max + n_grp_max + (int)Tm;
+  c->args.n_ctr_all = c->args.n_ctr_max + n_grp_max;
   size_t o_ctr = carve((size_t)c->args.n_ctr_all * 4);
   size_t o_srow = carve((size_t)c->R_cap * 4 + 4);
   size_t o_nu = carve(16);
@@ -350,7 +351,8 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
   a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
   a.sync = (int32_t *)(sb + o_sync); a.ctr = (int32_t *)(sb + o_ctr);
-  a.rdy = a.ctr + a.n_ctr_max; a.tokctr = a.rdy + n_grp_max; a.srcrow = (int32_t *)(sb + o_srow);
+  a.rdy = a.ctr + a.n_ctr_max; a.srcrow = (int32_t *)(sb + o_srow);
+  a.tokctr = reinterpret_cast<int32_t *>(c->sym + L.tokctr);
   a.n_units = (int32_t *)(sb + o_nu);
   a.H = (bf16 *)(sb + o_H); a.Hs = Fsh > 0 ? (bf16 *)(sb + o_Hs) : nullptr;
   a.ws = c->nsplit > 1 ? (float *)(sb + o_ws) : nullptr; a.ysh = Fsh > 0 ? (bf16 *)(sb + o_ysh) : nullptr;
@@ -699,7 +701,7 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
     const char *e = getenv("TG_LOCAL");
     const bool rows = !e || e[0] == '1' || e[0] == 'r', comb = !e || e[0] == '1' || e[0] == 'c';
     a.local_rows = c->world == 1 && rows;
-    a.local_comb = c->world == 1 && comb;
+    a.tok_comb = comb ? 1 : 0;
     const char *dv = getenv("TG_DEV");
     a.dev = dv ? atoi(dv) : 0;
   }
@@ -870,7 +872,7 @@ static tg_status replay_args(tg_ctx *c, const void *x, void *out, int T, CallArg
   a->sgate = c->sg_buf[c->last_wb];
   a->logits = nullptr;
   a->local_rows = 0;  // a replay is a multi-rank run (world > 1)
-  a->local_comb = 0;
+  a->tok_comb = 0;
   return TG_OK;
 }
 

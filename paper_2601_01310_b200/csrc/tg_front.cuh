@@ -679,6 +679,10 @@ __device__ void l2_prefetch_share(const CallArgs &a, int part, int nparts) {
 // phase counts on, and the counter set of the launch after next.
 __device__ __forceinline__ void post_wait_resets(const CallArgs &a) {
   for (int i = VBID * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += VGRID * blockDim.x) a.ctr[i] = 0;
+  // this rank's per-token arrival counters: the peers add to them only after this rank's dispatch
+  // (after the front's last grid barrier); the previous call's arrivals all landed before its combine
+  for (int i = VBID * blockDim.x + threadIdx.x; i < a.T; i += VGRID * blockDim.x) a.tokctr[i] = 0;
+  if (VBID == 0 && threadIdx.x == 0) a.sync[7] = 0;  // "combine incomplete" (a peer silent mid-call)
   const int nb = (a.cbuf + 2) % 3;
   for (int i = VBID * blockDim.x + threadIdx.x; i < a.gmax; i += VGRID * blockDim.x) a.grp_ctr[(size_t)nb * a.gmax + i] = 0;
   for (int i = VBID * blockDim.x + threadIdx.x; i < a.cmax; i += VGRID * blockDim.x) a.chunk_ctr[(size_t)nb * a.cmax + i] = 0;

@@ -664,7 +664,9 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
         }
         tc_fence_before();
         mbar_arrive(&S->tempty[h]);
-        if (direct) named_bar_sync(1, 128);  // the table is rebuilt by the next unit
+        const bool arrive = a.tok_comb && !split;
+        if (arrive) fence_scope(sys);  // this thread's y / y_sh stores (peer memory too) before the arrivals
+        if (direct || (arrive && sh)) named_bar_sync(1, 128);  // every store of the unit done; table reusable
         if (split) {
           // fixed-order split-K reduction ((p0 + p1) + p2) + ... by the last split to finish
           __threadfence();
@@ -723,17 +725,26 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
             }
             }
           }
+          if (a.tok_comb && S->red_last) fence_scope(sys);  // the reduced y rows before the arrivals
           named_bar_sync(1, 128);
         }
-        if (a.local_comb && (!split || S->red_last)) {
-          // per-token arrivals (one per unit storing a token's outputs): the combine below starts
-          // a token as soon as all k (+ shared) outputs over every c-tile are stored, without a
-          // grid barrier after the GEMM
-          if (sh) named_bar_sync(1, 128);  // every y_sh store of the unit done
-          __threadfence();
-          for (int i = et; i < U.nrows; i += 128)  // token tiles of up to 256 (wide mode)
-            atomicAdd(a.tokctr + (sh ? U.n0 - a.R_sh0 + i : meta[U.n0 + i].y / a.k),
-                      (U.dual && U.m0 + BM < a.d) ? 2 : 1);
+        if (a.tok_comb && (!split || S->red_last)) {
+          // per-token arrivals at the token's source AW (its counter is in the peer-visible region:
+          // an NVLink atomic when the source is a peer), one per 128-column output tile stored: the
+          // source combines a token as soon as all k (+ shared) outputs over every c-tile are stored,
+          // without a grid barrier after the GEMM
+          const int add = (U.dual && U.m0 + BM < a.d) ? 2 : 1;
+          for (int i = et; i < U.nrows; i += 128) {  // token tiles of up to 256 (wide mode)
+            int src = a.rank, t = U.n0 - a.R_sh0 + i;
+            if (!sh) {
+              const int2 o = meta[U.n0 + i];
+              src = o.x;
+              t = o.y / a.k;
+            }
+            int *c = reinterpret_cast<int *>(a.sym[src] + a.L.tokctr) + t;
+            if (src == a.rank || !sys) atomicAdd(c, add);
+            else atomicAdd_system(c, add);
+          }
         }
       }
       if (a.trace && et == 0) {
@@ -752,18 +763,53 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
   }
 
   // ===================== combine (GK5), all CTAs =====================
-  if (a.local_comb) {
-    // warp per token, grid-stride from this CTA's warps as soon as its GEMM work is done: a
-    // token is combined once its arrival count is complete (no grid barrier); a lane owns
-    // d / 256 chunks of 8 outputs, all their loads in flight
-    // arrivals count 128-column output tiles (a dual unit stores two; d % 256 == 0 when dual)
+  if (a.tok_comb) {
+    const uint32_t part = (uint32_t)__ldcg(a.sync + 6);
+    if (a.world > 1) {
+      // the last CTA of this rank to finish its GEMM work releases the combine flags: every expert
+      // output this rank computed is in its source's combine buffer (failure detection, below)
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_scope(sys);
+        if (atomicAdd(a.sync + 2, 1) == VGRID - 1) {
+          fence_scope(sys);
+          for (int q = 0; q < a.world; ++q)
+            if ((part >> q) & 1u)
+              st_release(reinterpret_cast<uint32_t *>(a.sym[q] + a.L.flags) + a.fslot_comb * kMaxWorld + a.rank,
+                         a.fepoch, sys);
+        }
+      }
+    }
+    // warp per token, grid-stride from this CTA's warps as soon as its GEMM work is done: a token
+    // is combined once its arrival count is complete (no grid barrier: the combine runs beside the
+    // GEMM tail on every rank); a lane owns d / 256 chunks of 8 outputs, all their loads in flight.
+    // Arrivals count 128-column output tiles (a dual unit stores two; d % 256 == 0 when dual).
     const int target = (a.k + (a.Fsh > 0 ? 1 : 0)) * ((a.d + BM - 1) / BM);
+    const uint32_t wmask = (a.world >= 32) ? 0xffffffffu : ((1u << a.world) - 1u);
+    const uint32_t live = (a.alive | (1u << a.rank)) & wmask;
     const bf16 *ybuf = reinterpret_cast<const bf16 *>(a.sym[a.rank] + a.L.ybuf);
-    for (int t = VBID * 8 + warp; t < a.T; t += VGRID * 8) {
-      if (lane == 0) wait_ctr_ge(a.tokctr + t, target, err, 0x5002);
-      __syncwarp();
-      __threadfence();
-      for (int c0 = lane; c0 < (a.d >> 3); c0 += 4 * 32) combine_chunks<4>(a, ybuf, t, c0, 32);
+    if ((part & wmask) == live) {  // (a peer failed in the count exchange: pairs were not sent, tg_failover redoes it)
+      for (int t = VBID * 8 + warp; t < a.T; t += VGRID * 8) {
+        int ok = 1;
+        if (lane == 0) {
+          if (a.world == 1) {
+            wait_ctr_ge(a.tokctr + t, target, err, 0x5002);
+          } else if (ld_acquire_gpu(a.sync + 7) || !wait_ctr_or_fail(a.tokctr + t, target, sys, a.fail_timeout_ns)) {
+            ok = 0;  // a peer fell silent mid-call: the combine is left to tg_failover
+            atomicExch(a.sync + 7, 1);
+          }
+        }
+        if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+        fence_scope(sys);
+        for (int c0 = lane; c0 < (a.d >> 3); c0 += 4 * 32) combine_chunks<4>(a, ybuf, t, c0, 32);
+      }
+    }
+    // every live rank waits for every other live rank's combine flag (not only the EWs it sent
+    // rows to), so all survivors see a rank that fails mid-call in the same call (§5.1)
+    if (a.world > 1 && VBID == 0 && threadIdx.x < a.world && threadIdx.x != a.rank && ((part >> threadIdx.x) & 1u)) {
+      const uint32_t *fl =
+          reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) + a.fslot_comb * kMaxWorld + threadIdx.x;
+      if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns)) atomicOr(a.fail_mask, 1u << threadIdx.x);
     }
     return;
   }

@@ -76,6 +76,7 @@ struct SymLayout {
   size_t dup;       // int32 [R_cap]              token dedup: recv row to copy this row from (-1: sent)
   size_t ybuf;      // bf16 [T_max][k][d]         expert outputs returned to this AW
   size_t cnt_all;   // int32 [3][world][nkeys]    all-gathered per-source counts (calls by parity, replays)
+  size_t tokctr;    // int32 [T_max]              per-token arrival counters (EW epilogues add, AW combines)
   size_t flags;     // uint32 [6][kMaxWorld]      cnt / data / comb epoch flags; replay data / comb / cnt
   size_t total;
 };
@@ -138,14 +139,15 @@ struct CallArgs {
                          // [6] ranks taking part in this run (alive and heard from in the count exchange);
                          // u64 grid barriers at [8], [10], [12]; [16 + cbuf] router item counters
   float *logits;         // [T_max][E_r] router logits of the last call (parity export; nullptr = off)
-  int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters, then rdy and tokctr
+  int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters, then rdy
   int n_ctr_max;
   int32_t *rdy;          // [n_grp_max] world == 1: rows of each token tile copied into recv
-  int32_t *tokctr;       // [T_max] world == 1: expert outputs (units) of each token stored
-  int n_ctr_all;         // ctr + rdy + tokctr entries (reset together at the start of a call)
+  int32_t *tokctr;       // [T_max] this rank's per-token arrival counters (peer-visible region: the EWs
+                         // that store a token's outputs add to its count, over NVLink when remote)
+  int n_ctr_all;         // ctr + rdy entries (reset together at the start of a call)
   int32_t *srcrow;       // [R_cap] world == 1: token of each received row
   int local_rows;        // world == 1: rows copied in row order beside the GEMM, per-tile counters
-  int local_comb;        // world == 1: per-token arrival counters, combine without a grid barrier
+  int tok_comb;          // per-token arrival counters, combine without a grid barrier (not in replays)
   int dev;               // development A/B switches (TG_DEV)
   int cta0, ncta;        // this rank's CTAs in the launch: [cta0, cta0 + ncta) (several virtual ranks
                          // of one GPU share one cooperative launch: tg_moe_layer_multi)

@@ -212,6 +212,22 @@ __device__ __forceinline__ bool wait_flag_or_fail(const uint32_t *flag, uint32_t
   return true;
 }
 
+// Wait until the counter reaches target; false after timeout_ns (a peer that should add to it
+// failed; no trap).  Scope-selected acquire (peers add with system-scope atomics over NVLink).
+__device__ __forceinline__ bool wait_ctr_or_fail(const int *ctr, int target, bool sys, long long timeout_ns) {
+  auto ld = [&]() {
+    int v;
+    if (sys) asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    else asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    return v;
+  };
+  if (ld() >= target) return true;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld() < target)
+    if ((long long)(globaltimer_ns() - t0) > timeout_ns) return false;
+  return true;
+}
+
 // Spin until *flag >= epoch (wrap-safe), bounded.
 __device__ __forceinline__ void wait_flag_ge(const uint32_t *flag, uint32_t epoch, int *err, int code) {
   if (static_cast<int32_t>(ld_acquire_sys(flag) - epoch) >= 0) return;
