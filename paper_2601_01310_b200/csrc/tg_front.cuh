@@ -688,6 +688,7 @@ __device__ __forceinline__ void post_wait_resets(const CallArgs &a) {
   for (int i = VBID * blockDim.x + threadIdx.x; i < a.cmax; i += VGRID * blockDim.x) a.chunk_ctr[(size_t)nb * a.cmax + i] = 0;
   if (VBID == 0 && threadIdx.x == 0) {
     *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
+    *reinterpret_cast<unsigned long long *>(a.sync + 10) = 0ull;  // the combine phase's barrier (replays)
     a.sync[16 + nb] = 0;
   }
   if (VBID == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;

@@ -813,8 +813,9 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
     }
     return;
   }
-  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 10);
-  grid_barrier(gbar, a.epoch, 1, 0, err, a.ncta);
+  // (failover replays and TG_LOCAL=0: barrier, combine flags, combine; the counter is zeroed per
+  // launch after griddepcontrol.wait — calls with the per-token combine never reach it)
+  grid_barrier_z(reinterpret_cast<unsigned long long *>(a.sync + 10), 0, err, a.ncta);
   if (a.trace && VBID == 0 && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 16] = globaltimer_ns();
   // combine flags: every rank taking part in this run waits for every other one (not only the
   // EWs it sent rows to), so all survivors see a rank that fails mid-run in the same run and

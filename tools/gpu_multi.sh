@@ -8,3 +8,4 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $G --mas
 for c in qwen_prefill mixtral_decode; do
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $G --master-addr 127.0.0.1 --master-port 29612 tools/nvlink_counters.py --config $c --W $((2*G)) > gpurun_out/mg${G}_nvlink_$c.json 2> gpurun_out/mg${G}_nvlink_$c.err
 done
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $G --master-addr 127.0.0.1 --master-port 29613 tools/trace_mp.py --config mixtral_decode > gpurun_out/mg${G}_trace_mixtral.jsonl 2> gpurun_out/mg${G}_trace.err
