@@ -80,6 +80,19 @@ struct tg_ctx {
   CallArgs args{};
   TmaMaps maps{};
   TmaMaps *maps_dev = nullptr;            // device copy (fused launches of virtual ranks)
+  // Two buffer sets used by alternate calls: call n+1 runs its front, dispatch and GEMM units on
+  // the SMs call n's tail frees (PDL, no griddepcontrol.wait), so nothing call n still uses may be
+  // touched by call n+1.  Call n-1, the last user of call n+1's set, has exited by then: a call
+  // triggers its dependents after its front's grid barrier, when all its CTAs (one per SM) are
+  // resident, i.e. when no CTA of the call before it is left.
+  struct SetState {
+    SymLayout L;
+    bf16 *H = nullptr, *Hs = nullptr, *ysh = nullptr;
+    float *ws = nullptr;
+    int32_t *ctr = nullptr, *srcrow = nullptr, *slot_rows = nullptr, *dbase = nullptr, *gcounts = nullptr,
+            *need_src = nullptr, *sent_to = nullptr, *sync = nullptr;
+  } set[2];
+  int last_set = 0;
   int *err_host = nullptr, *err_dev = nullptr;
   uint64_t *trace = nullptr;                     // device trace buffer (diagnostics)
   bool tracing = false;
@@ -167,6 +180,17 @@ static void resolve(tg_ctx *c) {
     }
     if (c->rkey[e] < 0) c->no_route = true;
   }
+}
+
+// Point a call's arguments at buffer set st (peer-visible layout and local scratch of the set).
+static void apply_set(tg_ctx *c, CallArgs *a, int st) {
+  const tg_ctx::SetState &S = c->set[st];
+  a->pset = st;
+  a->L = S.L;
+  a->H = S.H; a->Hs = S.Hs; a->ysh = S.ysh; a->ws = S.ws;
+  a->ctr = S.ctr; a->rdy = S.ctr + a->n_ctr_max; a->srcrow = S.srcrow; a->slot_rows = S.slot_rows;
+  a->dbase = S.dbase; a->gcounts = S.gcounts; a->need_src = S.need_src; a->sent_to = S.sent_to; a->sync = S.sync;
+  a->tokctr = c->sym ? reinterpret_cast<int32_t *>(c->sym + S.L.tokctr) : nullptr;
 }
 
 static tg_status make_map(tg_ctx *c, CUtensorMap *m, void *base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
@@ -278,14 +302,23 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   const size_t Tm = std::max(c->T_max, 1);
   SymLayout &L = c->L;
   size_t off = 0;
-  L.recv = off; off = align_up(off + (size_t)c->R_tot * d * 2, 1024);
-  L.meta = off; off = align_up(off + (size_t)c->R_tot * 8, 1024);
-  L.dup = off; off = align_up(off + (size_t)c->R_tot * 4, 1024);
-  L.ybuf = off; off = align_up(off + Tm * k * d * 2, 1024);
+  for (int st = 0; st < 2; ++st) {
+    SymLayout &Ls = c->set[st].L;
+    Ls.recv = off; off = align_up(off + (size_t)c->R_tot * d * 2, 1024);
+    Ls.meta = off; off = align_up(off + (size_t)c->R_tot * 8, 1024);
+    Ls.dup = off; off = align_up(off + (size_t)c->R_tot * 4, 1024);
+    Ls.ybuf = off; off = align_up(off + Tm * k * d * 2, 1024);
+    Ls.tokctr = off; off = align_up(off + Tm * 4, 1024);
+  }
+  L = c->set[0].L;
   L.cnt_all = off; off = align_up(off + (size_t)3 * world * c->nkeys * 4, 1024);
-  L.tokctr = off; off = align_up(off + Tm * 4, 1024);
   L.flags = off; off = align_up(off + kNumFlagKinds * kMaxWorld * 4, 1024);
   L.total = off;
+  for (int st = 0; st < 2; ++st) {
+    c->set[st].L.cnt_all = L.cnt_all;
+    c->set[st].L.flags = L.flags;
+    c->set[st].L.total = L.total;
+  }
   CKI(cudaMalloc(&c->sym, L.total));
   CKI(cudaMemset(c->sym, 0, L.total));
   c->peer[rank] = c->sym;
@@ -307,18 +340,26 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   size_t o_lp = carve(((Tm + 31) / 32) * (size_t)(d / 64) * 32 * (E + 1) * 4);  // groups * nkp * 32 * E floats (KP >= 64)
   const int gmax = (int)((Tm + 31) / 32), cmax = 1 + nblk_max;
   size_t o_gc2 = carve(3 * (size_t)gmax * 4), o_cc = carve(3 * (size_t)cmax * 4);
-  size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_dbase = carve(c->nkeys * 4), o_pos = carve(Tm * k * 4);
-  size_t o_gc = carve(c->nkeys * 4), o_need = carve(kMaxWorld * 4), o_sent = carve(kMaxWorld * 4);
-  size_t o_slot = carve(S_loc * 4), o_stats = carve((size_t)c->nkeys * 8), o_sync = carve(128);
+  size_t o_bcnt = carve((size_t)nblk_max * c->nkeys * 4), o_pos = carve(Tm * k * 4);
+  size_t o_stats = carve((size_t)c->nkeys * 8), o_gsync = carve(128);
   const int n_grp_max = nt_max + nt_sh + 16;
   c->args.n_ctr_all = c->args.n_ctr_max + n_grp_max;
-  size_t o_ctr = carve((size_t)c->args.n_ctr_all * 4);
-  size_t o_srow = carve((size_t)c->R_cap * 4 + 4);
   size_t o_nu = carve(16);
-  size_t o_H = carve((size_t)c->R_cap * F * 2);
-  size_t o_Hs = carve(Fsh > 0 ? Tm * Fsh * 2 : 0);
-  size_t o_ws = carve(c->nsplit > 1 ? (size_t)c->nsplit * c->R_cap * d * 4 : 0);
-  size_t o_ysh = carve(Fsh > 0 ? Tm * d * 2 : 0);
+  size_t o_set[2][12];
+  for (int st = 0; st < 2; ++st) {
+    o_set[st][0] = carve((size_t)c->args.n_ctr_all * 4);                                       // ctr
+    o_set[st][1] = carve((size_t)c->R_cap * 4 + 4);                                           // srcrow
+    o_set[st][2] = carve((size_t)c->R_cap * F * 2);                                           // H
+    o_set[st][3] = carve(Fsh > 0 ? Tm * Fsh * 2 : 0);                                         // Hs
+    o_set[st][4] = carve(c->nsplit > 1 ? (size_t)c->nsplit * c->R_cap * d * 4 : 0);           // ws
+    o_set[st][5] = carve(Fsh > 0 ? Tm * d * 2 : 0);                                           // ysh
+    o_set[st][6] = carve(c->nkeys * 4);                                                       // dbase
+    o_set[st][7] = carve(c->nkeys * 4);                                                       // gcounts
+    o_set[st][8] = carve(kMaxWorld * 4);                                                      // need_src
+    o_set[st][9] = carve(kMaxWorld * 4);                                                      // sent_to
+    o_set[st][10] = carve(S_loc * 4);                                                         // slot_rows
+    o_set[st][11] = carve(64);                                                                // sync
+  }
   size_t o_xs = carve(2 * Tm * d * 2), o_os = carve(2 * Tm * d * 2);
   CKI(cudaMalloc(&c->scratch, so));
   CKI(cudaMemset(c->scratch, 0, so));
@@ -347,20 +388,30 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   c->logits = (float *)(sb + o_lg);
   a.gate_mode = c->gate_mode; a.shared_gate = c->shared_gate; a.E_r = E + c->shared_gate; a.key = (int32_t *)(sb + o_key);
   c->key_main = a.key; c->key_replay = (int32_t *)(sb + o_key2);
-  a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.chunk_ctr = (int32_t *)(sb + o_cc); a.bcnt = (int32_t *)(sb + o_bcnt); a.dbase = (int32_t *)(sb + o_dbase);
-  a.dst_pos = (int32_t *)(sb + o_pos); a.gcounts = (int32_t *)(sb + o_gc); a.need_src = (int32_t *)(sb + o_need);
-  a.sent_to = (int32_t *)(sb + o_sent); a.slot_rows = (int32_t *)(sb + o_slot); a.stats = (int64_t *)(sb + o_stats);
-  a.sync = (int32_t *)(sb + o_sync); a.ctr = (int32_t *)(sb + o_ctr);
-  a.rdy = a.ctr + a.n_ctr_max; a.srcrow = (int32_t *)(sb + o_srow);
-  a.tokctr = reinterpret_cast<int32_t *>(c->sym + L.tokctr);
+  a.lrank = (int32_t *)(sb + o_lrank); a.logit_part = (float *)(sb + o_lp); a.grp_ctr = (int32_t *)(sb + o_gc2); a.chunk_ctr = (int32_t *)(sb + o_cc); a.bcnt = (int32_t *)(sb + o_bcnt);
+  a.dst_pos = (int32_t *)(sb + o_pos); a.stats = (int64_t *)(sb + o_stats);
+  a.gsync = (int32_t *)(sb + o_gsync);
   a.n_units = (int32_t *)(sb + o_nu);
-  a.H = (bf16 *)(sb + o_H); a.Hs = Fsh > 0 ? (bf16 *)(sb + o_Hs) : nullptr;
-  a.ws = c->nsplit > 1 ? (float *)(sb + o_ws) : nullptr; a.ysh = Fsh > 0 ? (bf16 *)(sb + o_ysh) : nullptr;
+  for (int st = 0; st < 2; ++st) {
+    tg_ctx::SetState &S = c->set[st];
+    S.ctr = (int32_t *)(sb + o_set[st][0]);
+    S.srcrow = (int32_t *)(sb + o_set[st][1]);
+    S.H = (bf16 *)(sb + o_set[st][2]);
+    S.Hs = Fsh > 0 ? (bf16 *)(sb + o_set[st][3]) : nullptr;
+    S.ws = c->nsplit > 1 ? (float *)(sb + o_set[st][4]) : nullptr;
+    S.ysh = Fsh > 0 ? (bf16 *)(sb + o_set[st][5]) : nullptr;
+    S.dbase = (int32_t *)(sb + o_set[st][6]);
+    S.gcounts = (int32_t *)(sb + o_set[st][7]);
+    S.need_src = (int32_t *)(sb + o_set[st][8]);
+    S.sent_to = (int32_t *)(sb + o_set[st][9]);
+    S.slot_rows = (int32_t *)(sb + o_set[st][10]);
+    S.sync = (int32_t *)(sb + o_set[st][11]);
+  }
+  apply_set(c, &a, 0);
   for (int i = 0; i < 2; ++i) {
     c->x_stage[i] = (bf16 *)(sb + o_xs) + (size_t)i * Tm * d;
     c->out_stage[i] = (bf16 *)(sb + o_os) + (size_t)i * Tm * d;
   }
-  a.L = L;
   {
     const char *e = getenv("TG_PDL");  // development switch for A/B timing; default on
     a.pdl = (e && e[0] == '0') ? 0 : 1;
@@ -389,16 +440,17 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   } else {
     c->maps.w1s = c->maps.w1; c->maps.w3s = c->maps.w3; c->maps.w2s = c->maps.w2;
   }
-  for (int i = 0; i < kNumBoxes; ++i) {
-    uint32_t br = 16 * (i + 1);
-    if ((s = make_map(c, &c->maps.x[i], c->sym + L.recv, c->R_tot, d, br)) != TG_OK) return bail(s);
-    if ((s = make_map(c, &c->maps.h[i], a.H, std::max(c->R_cap, 1), F, br)) != TG_OK) return bail(s);
-    if (Fsh > 0) {
-      if ((s = make_map(c, &c->maps.hs[i], a.Hs, Tm, Fsh, br)) != TG_OK) return bail(s);
-    } else {
-      c->maps.hs[i] = c->maps.h[i];
+  for (int st = 0; st < 2; ++st)
+    for (int i = 0; i < kNumBoxes; ++i) {
+      uint32_t br = 16 * (i + 1);
+      if ((s = make_map(c, &c->maps.x[st][i], c->sym + c->set[st].L.recv, c->R_tot, d, br)) != TG_OK) return bail(s);
+      if ((s = make_map(c, &c->maps.h[st][i], c->set[st].H, std::max(c->R_cap, 1), F, br)) != TG_OK) return bail(s);
+      if (Fsh > 0) {
+        if ((s = make_map(c, &c->maps.hs[st][i], c->set[st].Hs, Tm, Fsh, br)) != TG_OK) return bail(s);
+      } else {
+        c->maps.hs[st][i] = c->maps.h[st][i];
+      }
     }
-  }
   CKI(cudaMalloc(&c->maps_dev, sizeof(TmaMaps)));
   CKI(cudaMemcpy(c->maps_dev, &c->maps, sizeof(TmaMaps), cudaMemcpyHostToDevice));
   CKI(layer_configure());
@@ -633,12 +685,13 @@ tg_status tg_get_stage(tg_ctx *c, int stage, void *dst, size_t cap, size_t *byte
   CK(cudaDeviceSynchronize());
   tg_status st = check_sticky(c);
   if (st) return st;
-  const CallArgs &a = c->args;
+  const tg_ctx::SetState &LS = c->set[c->last_set];  // the last call's buffer set
   const size_t T = (size_t)c->last_T;
   size_t R = 0;
   if (stage == TG_STAGE_RECV || stage == TG_STAGE_META || stage == TG_STAGE_H) {
     std::vector<int32_t> rows(std::max(c->S_loc, 1), 0);
-    if (c->S_loc) CK(cudaMemcpy(rows.data(), a.slot_rows, sizeof(int32_t) * c->S_loc, cudaMemcpyDeviceToHost));
+    if (c->S_loc)
+      CK(cudaMemcpy(rows.data(), c->set[c->last_set].slot_rows, sizeof(int32_t) * c->S_loc, cudaMemcpyDeviceToHost));
     for (int i = 0; i < c->S_loc; ++i) R += (size_t)rows[i];
   }
   const void *src = nullptr;
@@ -647,12 +700,12 @@ tg_status tg_get_stage(tg_ctx *c, int stage, void *dst, size_t cap, size_t *byte
     case TG_STAGE_LOGITS:
       if (!c->stage_export) return fail(c, TG_ERR_INVALID, "logits are exported only after tg_set_stage_export(ctx, 1)");
       src = c->logits; n = T * (size_t)(c->E + c->shared_gate) * 4; break;
-    case TG_STAGE_RECV: src = c->sym + c->L.recv; n = R * c->d * 2; break;
-    case TG_STAGE_META: src = c->sym + c->L.meta; n = R * 8; break;
-    case TG_STAGE_H: src = a.H; n = R * c->F * 2; break;
-    case TG_STAGE_Y: src = c->sym + c->L.ybuf; n = T * c->k * c->d * 2; break;
-    case TG_STAGE_HSH: src = a.Hs; n = c->Fsh ? T * c->Fsh * 2 : 0; break;
-    case TG_STAGE_YSH: src = a.ysh; n = c->Fsh ? T * c->d * 2 : 0; break;
+    case TG_STAGE_RECV: src = c->sym + LS.L.recv; n = R * c->d * 2; break;
+    case TG_STAGE_META: src = c->sym + LS.L.meta; n = R * 8; break;
+    case TG_STAGE_H: src = LS.H; n = R * c->F * 2; break;
+    case TG_STAGE_Y: src = c->sym + LS.L.ybuf; n = T * c->k * c->d * 2; break;
+    case TG_STAGE_HSH: src = LS.Hs; n = c->Fsh ? T * c->Fsh * 2 : 0; break;
+    case TG_STAGE_YSH: src = LS.ysh; n = c->Fsh ? T * c->d * 2 : 0; break;
     case TG_STAGE_SGATE: src = c->sg_buf[c->last_wb]; n = c->shared_gate ? T * 4 : 0; break;
     default: return fail(c, TG_ERR_INVALID, "unknown stage %d", stage);
   }
@@ -749,6 +802,8 @@ static tg_status prepare_call(tg_ctx *c, const void *x, void *out, int T, CallAr
   c->last_wb = (int)(a->xepoch & 1);
   a->w = c->w_buf[c->last_wb];
   a->sgate = c->sg_buf[c->last_wb];
+  apply_set(c, a, c->last_wb);
+  c->last_set = c->last_wb;
   a->inject_fail = c->inject_next ? 1 : 0;
   c->inject_next = false;
   return TG_OK;
@@ -870,6 +925,7 @@ static tg_status replay_args(tg_ctx *c, const void *x, void *out, int T, CallArg
   a->key = c->key_replay;
   a->w = c->w_buf[c->last_wb];  // the failed call's gate weights (its combine is redone)
   a->sgate = c->sg_buf[c->last_wb];
+  apply_set(c, a, c->last_set);  // and its buffer set: the other pairs' outputs are kept
   a->logits = nullptr;
   a->local_rows = 0;  // a replay is a multi-rank run (world > 1)
   a->tok_comb = 0;
@@ -1027,7 +1083,7 @@ tg_status tg_get_routing(tg_ctx *c, int n_tokens, int32_t *idx, float *w, int32_
   if (idx && n) CK(cudaMemcpyAsync(idx, c->args.idx, n * 4, cudaMemcpyDeviceToDevice, s));
   if (w && n) CK(cudaMemcpyAsync(w, c->w_buf[c->last_wb], n * 4, cudaMemcpyDeviceToDevice, s));
   if (dst_pos && n) CK(cudaMemcpyAsync(dst_pos, c->args.dst_pos, n * 4, cudaMemcpyDeviceToDevice, s));
-  if (counts) CK(cudaMemcpyAsync(counts, c->args.gcounts, (size_t)c->nkeys * 4, cudaMemcpyDeviceToDevice, s));
+  if (counts) CK(cudaMemcpyAsync(counts, c->set[c->last_set].gcounts, (size_t)c->nkeys * 4, cudaMemcpyDeviceToDevice, s));
   if ((dst_rank || dst_slot) && n) CK(launch_export_keys(c->args, (int)n, dst_rank, dst_slot, s));
   return TG_OK;
 }

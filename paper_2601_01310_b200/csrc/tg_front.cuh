@@ -614,7 +614,6 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
   }
   __syncthreads();
   if (!s_last) return;
-  griddep_wait();  // the exchange and everything after it touch state the previous call may use
   TG_STAMP_ANY(1);
   exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(sm));
   TG_STAMP_ANY(14);
@@ -687,9 +686,9 @@ __device__ __forceinline__ void post_wait_resets(const CallArgs &a) {
   for (int i = VBID * blockDim.x + threadIdx.x; i < a.gmax; i += VGRID * blockDim.x) a.grp_ctr[(size_t)nb * a.gmax + i] = 0;
   for (int i = VBID * blockDim.x + threadIdx.x; i < a.cmax; i += VGRID * blockDim.x) a.chunk_ctr[(size_t)nb * a.cmax + i] = 0;
   if (VBID == 0 && threadIdx.x == 0) {
-    *reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
+    *reinterpret_cast<unsigned long long *>(a.gsync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
     *reinterpret_cast<unsigned long long *>(a.sync + 10) = 0ull;  // the combine phase's barrier (replays)
-    a.sync[16 + nb] = 0;
+    a.gsync[16 + nb] = 0;
   }
   if (VBID == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
 }
@@ -701,13 +700,13 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   // grid barriers of this call count on sync[8 + 4 * (epoch & 1)] (u64) from 0; the other
   // counter is reset here for the next call (the previous call has completed: PDL wait
   // at kernel entry)
-  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
+  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.gsync + 8 + 4 * (a.epoch & 1));
   int nbar = 0;
   TG_STAMP(0);
   // ---- P1 router: router items go to the CTAs in the order they start (under PDL the first
   // ones start on the SMs the previous call's tail frees)
   __shared__ int s_item;
-  if (threadIdx.x == 0) s_item = atomicAdd(a.sync + 16 + a.cbuf, 1);
+  if (threadIdx.x == 0) s_item = atomicAdd(a.gsync + 16 + a.cbuf, 1);
   __syncthreads();
   const int bitem = s_item;
   TG_STAMP(8);
@@ -757,7 +756,6 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     // CTAs after their items (and their top-k chains), the idle ones after a short delay
     if (!(slot < bpp && slot < ngroups)) __nanosleep(2000);
     l2_prefetch_share(a, bitem, VGRID);
-    griddep_wait();
     post_wait_resets(a);
     if (!chain) {
       const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
@@ -802,7 +800,7 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
 // so the replay rows are the whole work list of the destination EWs ("replayed
 // requests are prioritized").
 __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys &rk, uint8_t *fsm) {
-  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.sync + 8 + 4 * (a.epoch & 1));
+  unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.gsync + 8 + 4 * (a.epoch & 1));
   griddep_wait();
   post_wait_resets(a);
   int nbar = 0;

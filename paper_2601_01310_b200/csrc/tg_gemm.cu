@@ -283,7 +283,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
     a.trace[a.n_units_max + 148 + 19] = a.trace[a.n_units_max + 148 + 17];
     a.trace[a.n_units_max + 148 + 18] = globaltimer_ns();
   }
-  // PDL: the front waits (griddepcontrol.wait) before it touches state of the previous call
+  // PDL: this call may run beside the previous one's tail (its buffer set is the other one)
   // ===================== front: P1 router .. P3 count exchange (tg_front.cuh) =====================
   if (a.replay) replay_front(a, rk, smem_raw);
   else front_phase(a, rk, smem_raw);
@@ -443,7 +443,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
         const int kps = max(1, (int)(stage_bytes / sub));  // K blocks per stage (2 for decode GEMM2)
         const CUtensorMap *mA0 = g1 ? (sh ? &maps.w1s : &maps.w1) : (sh ? &maps.w2s : &maps.w2);
         const CUtensorMap *mA1 = sh ? &maps.w3s : &maps.w3;
-        const CUtensorMap *mB = g1 ? &maps.x[bi] : (sh ? &maps.hs[bi] : &maps.h[bi]);
+        const CUtensorMap *mB = g1 ? &maps.x[a.pset][bi] : (sh ? &maps.hs[a.pset][bi] : &maps.h[a.pset][bi]);
         const int rowA = g1 ? U.slot * (sh ? a.Fsh : a.F) + U.m0 : U.slot * a.d + U.m0;
         const int rowB = (!g1 && sh) ? U.n0 - a.R_sh0 : U.n0;
         const uint64_t pol_w = (U.ntiles > 1) ? pol_wn : pol_w1;
@@ -804,6 +804,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
         for (int c0 = lane; c0 < (a.d >> 3); c0 += 4 * 32) combine_chunks<4>(a, ybuf, t, c0, 32);
       }
     }
+    __threadfence();  // this call's stores before the call after next reuses its buffer set
     // every live rank waits for every other live rank's combine flag (not only the EWs it sent
     // rows to), so all survivors see a rank that fails mid-call in the same call (§5.1)
     if (a.world > 1 && VBID == 0 && threadIdx.x < a.world && threadIdx.x != a.rank && ((part >> threadIdx.x) & 1u)) {

@@ -63,13 +63,15 @@ struct Unit {
 struct TmaMaps {
   CUtensorMap w1, w3, w2;          // expert bank
   CUtensorMap w1s, w3s, w2s;       // shared expert
-  CUtensorMap x[kNumBoxes];        // receive buffer, box rows 16*(i+1)
-  CUtensorMap h[kNumBoxes];        // SwiGLU activations H, box rows 16*(i+1)
-  CUtensorMap hs[kNumBoxes];       // shared-expert activations
+  CUtensorMap x[2][kNumBoxes];     // receive buffer of each buffer set, box rows 16*(i+1)
+  CUtensorMap h[2][kNumBoxes];     // SwiGLU activations H of each set, box rows 16*(i+1)
+  CUtensorMap hs[2][kNumBoxes];    // shared-expert activations of each set
 };
 
 // Peer-visible ("symmetric") region: same layout and size on every rank, one
-// CUDA IPC handle per rank.  Offsets in bytes.
+// CUDA IPC handle per rank.  Offsets in bytes.  recv / meta / dup / ybuf / tokctr exist once per
+// buffer set (two sets, used by alternate calls: consecutive calls overlap); a call's CallArgs
+// carries the layout of its set.
 struct SymLayout {
   size_t recv;      // bf16 [R_cap][d]            dispatched token rows
   size_t meta;      // int2 [R_cap]               origin (src rank, t*k + j)
@@ -135,9 +137,12 @@ struct CallArgs {
   int32_t *sent_to;      // [kMaxWorld] this rank sends rows to dest
   int32_t *slot_rows;    // [S_loc] M_s on this rank
   int64_t *stats;        // [nkeys]
-  int32_t *sync;         // [0..4] counters (scheduler, CTAs done, dispatch blocks, -, dedup copies), [5] dedup on,
-                         // [6] ranks taking part in this run (alive and heard from in the count exchange);
-                         // u64 grid barriers at [8], [10], [12]; [16 + cbuf] router item counters
+  int32_t *sync;         // this call's buffer set: [0..4] counters (scheduler, CTAs done, dispatch blocks, -,
+                         // dedup copies), [5] dedup on, [6] ranks taking part in this run (alive and heard
+                         // from in the count exchange), [7] combine incomplete; u64 combine barrier at [10]
+  int32_t *gsync;        // shared by all calls: u64 front grid barriers at [8], [12] (by launch parity);
+                         // [16 + cbuf] router item counters
+  int pset;              // buffer set of this call (call parity; a failover replay: the failed call's)
   float *logits;         // [T_max][E_r] router logits of the last call (parity export; nullptr = off)
   int32_t *ctr;          // [n_ctr_max] GEMM dependency / reduction counters, then rdy
   int n_ctr_max;

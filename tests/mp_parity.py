@@ -269,9 +269,11 @@ def inflight_fail_checks(tg, layer, rank, world, out, run, xr, msgs, rep):
 def finish(ok, rank, rep, msgs, layer, dev):
     flags = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flags)
+    all_msgs = [None] * dist.get_world_size()
+    dist.all_gather_object(all_msgs, msgs)  # every rank's messages, not only rank 0's
     if rank == 0:
         rep["ok"] = bool(flags.item() == 0)
-        rep["errors"] = msgs
+        rep["errors"] = [m for ms in all_msgs for m in ms]
         print(json.dumps(rep), flush=True)
     layer.close()
     dist.barrier()
