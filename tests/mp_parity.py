@@ -56,7 +56,8 @@ def main():
     pl = wl.make_placement(sh.E, W, world)
     layer = tg.MoELayer(sh, pl, L, max_tokens_per_rank=Tr, rank=rank, world=world, device=local,
                         group=dist.group.WORLD)
-    layer.export_stages(True)
+    if os.environ.get("TG_NO_EXPORT") != "1":
+        layer.export_stages(True)
     xr = x[rank * Tr:(rank + 1) * Tr].contiguous().to(dev)
     rep = {"rank": rank, "world": world, "W": W, "config": a.config, "T": T}
     ok = True
@@ -93,7 +94,12 @@ def main():
     out2 = run()
     if not torch.equal(out.view(torch.int16), out2.view(torch.int16)):
         ok = False
-        msgs.append(f"rank {rank}: run-to-run differs")
+        dif = out.view(torch.int16) != out2.view(torch.int16)
+        toks = dif.any(dim=1).nonzero().flatten()
+        same_as_gathered = bool(torch.equal(out2.cpu().view(torch.int16),
+                                            out_all[rank * Tr:(rank + 1) * Tr].view(torch.int16)))
+        msgs.append(f"rank {rank}: run-to-run differs ({int(dif.sum())} elements, tokens {toks[:6].tolist()} of "
+                    f"{int(toks.numel())}; second call equal to the gathered first: {same_as_gathered})")
     if a.rank_fail:
         ok = rank_fail_checks(a, tg, layer, pl, sh, W, rank, world, dev, out, run, msgs, rep) and ok
         finish(ok, rank, rep, msgs, layer, dev)
