@@ -415,6 +415,8 @@ def main():
     group = None
     if N > 1:
         import torch.distributed as dist
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"  # the version banner goes to stdout: one JSON line only
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
     local_experts = sorted({e for ew in range(W) if pl.ew_rank[ew] == rank for e in pl.hosted[ew] if e >= 0})
