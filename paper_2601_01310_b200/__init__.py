@@ -360,6 +360,11 @@ def tg_get_trace(ctx, cap=1 << 20):
                 front_stamps=(tr[nu + 148:nu + 148 + 64] & m48).astype(np.int64),
                 front_stamps_raw=tr[nu + 148:nu + 148 + 64].astype(np.int64),
                 front_block_p1=(tr[nu + 148 + 64:nu + 148 + 64 + 148] & m48).astype(np.int64),
+                front_block_router=(tr[nu + 148 + 64 + 552:nu + 148 + 64 + 700] & m48).astype(np.int64),
+                front_block_prefetch=(tr[nu + 148 + 64 + 700:nu + 148 + 64 + 848] & m48).astype(np.int64),
+                topk_detail=tr[nu + 148 + 64 + 1000:nu + 148 + 64 + 1012].astype(np.int64),
+                item_clock=tr[nu + 148 + 64 + 1012:nu + 148 + 64 + 1016].astype(np.int64),
+                front_block_bar1=(tr[nu + 148 + 64 + 848:nu + 148 + 64 + 996] & m48).astype(np.int64),
                 topk_cycles=tr[nu + 148 + 64 + 256:nu + 148 + 64 + 256 + 296].astype(np.int64).reshape(148, 2))
 
 

@@ -754,7 +754,13 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
     const char *e = getenv("TG_LOCAL");
     const bool rows = !e || e[0] == '1' || e[0] == 'r', comb = !e || e[0] == '1' || e[0] == 'c';
     a.local_rows = c->world == 1 && rows;
-    a.tok_comb = comb ? 1 : 0;
+    // world > 1: each (pair, pair of 128-column output tiles) is one NVLink atomic at its source;
+    // past ~48K per rank the grid-barrier combine wins (2-GPU A/B, µs per call, per-token vs
+    // barrier: Mixtral decode 293 vs 302 (4K arrivals), DS-V2-Lite decode 196 vs 208 (25K), Qwen
+    // prefill 521 vs 464 (131K)).  Static per ctx (T_max, k, d agree on every rank): the EWs'
+    // arrivals and the sources' waits must take the same branch.
+    const long arrivals = (long)c->T_max * c->k * ((c->d + 2 * BM - 1) / (2 * BM));
+    a.tok_comb = comb && (c->world == 1 || arrivals <= kTokCombMaxArrivals) ? 1 : 0;
     const char *dv = getenv("TG_DEV");
     a.dev = dv ? atoi(dv) : 0;
   }

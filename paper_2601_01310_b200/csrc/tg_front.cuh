@@ -159,6 +159,59 @@ __device__ __forceinline__ void router_issue(const CallArgs &a, const RouterSmem
 // sets of 8 k16 steps, each in its own fp32 registers, the sets summed in fp64 in K order
 // (shorter fp32 chains: ~1 ulp of logit instead of several), sub-slices likewise through smem;
 // the part's sum is stored rounded to fp32.  Order fixed by (d, E): deterministic, row-invariant.
+//
+// Fast path for KP = 512 and 8 expert tiles (E_r in 57..64: the DS-V2-Lite and Qwen shapes):
+// warp w owns the m16 block w & 1 and the n8 tiles 2 (w >> 1), +1 (A fragments loaded once per
+// two tiles), the 32 k16 steps in compile-time order with every fragment loaded two steps ahead
+// of its mma (ldmatrix / mma are volatile asm: program order is issue order, so the schedule is
+// written out here).  Per logit the arithmetic is the generic path's — set q = steps 8q..8q+7 in
+// order, one m16n8k16 per step, sets summed in fp64 in q order — so the results are identical.
+__device__ __forceinline__ void router_compute_k512_t8(const CallArgs &a, const RouterSmem &R, int grp, int kp,
+                                                       int buf) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = a.E_r, nkp = router_nkp(a.d, E);
+  const int g = lane >> 2, c = lane & 3, mb = warp & 1, t0 = 2 * (warp >> 1);
+  const uint32_t *xb = R.xt + (size_t)buf * kRouterRows * R.ldw;
+  const uint32_t xa = smem_u32(xb + (16 * mb + (lane & 15)) * R.ldw) + (lane >> 4) * 16;
+  const uint32_t wa0 = smem_u32(R.wg + (t0 * 8 + (lane & 7)) * R.ldw) + ((lane >> 3) & 1) * 16;
+  const uint32_t wa1 = wa0 + 8 * R.ldw * 4;
+  float acc[4][2][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[q][t][i] = 0.f;
+  // issue order s = 4 st + q (k16 step q * 8 + st), fragments in a 3-deep register ring
+  uint32_t fa[3][4], fb[3][4];
+  auto load = [&](int s, int r) {
+    const uint32_t off = (uint32_t)((s & 3) * 8 + (s >> 2)) * 32;
+    ldsm_x4(fa[r], xa + off);
+    ldsm_x2(fb[r][0], fb[r][1], wa0 + off);
+    ldsm_x2(fb[r][2], fb[r][3], wa1 + off);
+  };
+  load(0, 0);
+  load(1, 1);
+#pragma unroll
+  for (int s = 0; s < 32; ++s) {
+    if (s + 2 < 32) load(s + 2, (s + 2) % 3);
+    const int r = s % 3, q = s & 3;
+    mma_bf16_16816(acc[q][0], fa[r], fb[r][0], fb[r][1]);
+    mma_bf16_16816(acc[q][1], fa[r], fb[r][2], fb[r][3]);
+  }
+  float *dst = a.logit_part + ((size_t)grp * nkp + kp) * kRouterRows * E;
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double sum = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sum += (double)acc[q][t][i];
+      const int row = 16 * mb + g + 8 * (i >> 1), e = (t0 + t) * 8 + 2 * c + (i & 1);
+      if (e < E) dst[row * E + e] = (float)sum;
+    }
+}
+
 __device__ __forceinline__ void router_compute(const CallArgs &a, const RouterSmem &R, int grp, int kp, int buf) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = a.d, E = a.E_r;
@@ -166,6 +219,10 @@ __device__ __forceinline__ void router_compute(const CallArgs &a, const RouterSm
   const int KP = router_kpart(d, E), nkp = router_nkp(d, E);
   const int ntl = router_ntiles(E), nsub = router_nsub(d, E), nte = min(ntl, 8);
   const int steps = KP / 16 / nsub;               // k16 steps of one sub-slice
+  if (KP == 512 && ntl == 8 && nsub == 1) {
+    router_compute_k512_t8(a, R, grp, kp, buf);
+    return;
+  }
   const uint32_t *xb = R.xt + (size_t)buf * kRouterRows * R.ldw;
   float *dst = a.logit_part + ((size_t)grp * nkp + kp) * kRouterRows * E;
   for (int eb = 0; eb < ntl; eb += 8) {          // expert blocks of 8 n8 tiles (E > 64)
@@ -283,8 +340,9 @@ __device__ __forceinline__ bool beats(float v, int e, float v2, int e2) {
 // j-th pick.
 template <int PER>
 __device__ __forceinline__ void topk_rows(const CallArgs &a, const RouteKeys &rk, int t0, bool act,
-                                          const float *l, int *rsl) {
+                                          const float *l, int *rsl, uint64_t *cyc = nullptr) {
   const int E = a.E, k = a.k, lane = threadIdx.x & 31, sub = lane & 7;
+  if (cyc && threadIdx.x == 0) cyc[0] = clock64();
   const int r = threadIdx.x >> 3;
   float v[PER];
 #pragma unroll
@@ -319,6 +377,7 @@ __device__ __forceinline__ void topk_rows(const CallArgs &a, const RouteKeys &rk
     if (sub == j) { mine = be; mval = bv; }
     if (j == 0) m = bv;  // top-1 logit = max of the selected
   }
+  if (cyc && threadIdx.x == 0) cyc[1] = clock64();
   // slot = picks with a smaller id (ascending expert id, R#4)
   int slot = 0;
 #pragma unroll 1
@@ -340,6 +399,7 @@ __device__ __forceinline__ void topk_rows(const CallArgs &a, const RouteKeys &rk
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
   }
+  if (cyc && threadIdx.x == 0) cyc[2] = clock64();
   if (act) {
     const int t = t0 + r;
     if (sub < k) {
@@ -350,53 +410,72 @@ __device__ __forceinline__ void topk_rows(const CallArgs &a, const RouteKeys &rk
     }
     if (a.shared_gate && sub == 0) a.sgate[t] = __fdiv_rn(1.0f, 1.0f + expf(-l[E]));  // router row E
   }
+  if (cyc && threadIdx.x == 0) cyc[3] = clock64();
 }
 
-__device__ __forceinline__ void group_topk(const CallArgs &a, const RouteKeys &rk, int grp, float *sm) {
-  const int Er = a.E_r, E = a.E, nkp = router_nkp(a.d, Er), ld = Er + 1;  // padded rows
-  const int t0 = grp * kRouterRows, nrow = min(kRouterRows, a.T - t0);
-  const int n = nrow * Er;
-  const float *src = a.logit_part + (size_t)grp * nkp * kRouterRows * Er;
-  float *lsum = sm;                                              // [32][Er + 1]
-  int *sl = reinterpret_cast<int *>(lsum + kRouterRows * ld);    // [32][kMaxK] selected ids by slot
+template <int U, int Q>
+__device__ __forceinline__ void gather_parts(const float *src, size_t pstride, int n, int nkp, int Er, float *lsum) {
   const int bd = blockDim.x;
 #pragma unroll 1
-  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * bd) {
-    double s[4] = {0.0, 0.0, 0.0, 0.0};  // parts summed in fp64 in part order, rounded once
+  for (int i0 = threadIdx.x; i0 < n; i0 += U * bd) {
+    double s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[u] = 0.0;
 #pragma unroll 1
-    for (int q0 = 0; q0 < nkp; q0 += 4) {
-      float p[4][4];
+    for (int q0 = 0; q0 < nkp; q0 += Q) {
+      float p[U][Q];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int q = 0; q < Q; ++q) {
+        const float *pq = src + (size_t)min(q0 + q, nkp - 1) * pstride;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          p[u][q] = (i0 + u * bd < n && q0 + q < nkp)
-                        ? __ldcg(src + (size_t)(q0 + q) * kRouterRows * Er + i0 + u * bd) : 0.f;
+        for (int u = 0; u < U; ++u) p[u][q] = __ldcg(pq + min(i0 + u * bd, n - 1));
+      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < Q; ++q)
           if (q0 + q < nkp) s[u] += (double)p[u][q];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int i = i0 + u * bd;
       if (i < n) lsum[i + i / Er] = (float)s[u];  // row i / Er, padded stride Er + 1
     }
   }
+}
+
+__device__ __forceinline__ void group_topk(const CallArgs &a, const RouteKeys &rk, int grp, float *sm,
+                                           uint64_t *cyc = nullptr) {
+  if (cyc && threadIdx.x == 0) cyc[4] = clock64();
+  const int Er = a.E_r, E = a.E, nkp = router_nkp(a.d, Er), ld = Er + 1;  // padded rows
+  const int t0 = grp * kRouterRows, nrow = min(kRouterRows, a.T - t0);
+  const int n = nrow * Er;
+  const size_t pstride = (size_t)kRouterRows * Er;  // one K part of the group
+  const float *src = a.logit_part + (size_t)grp * nkp * pstride;
+  float *lsum = sm;                                              // [32][Er + 1]
+  int *sl = reinterpret_cast<int *>(lsum + kRouterRows * ld);    // [32][kMaxK] selected ids by slot
+  const int bd = blockDim.x;
+  // Parts summed in fp64 in part order, rounded once.  Every load of a round is issued before
+  // the first sum: unconditional loads from clamped addresses (a predicated load whose value
+  // is consumed at once serialises the round on its latency), out-of-range values unused.
+  // U elements x Q parts per thread and round, by the group's size (decode: one element).
+  if (n <= bd) gather_parts<1, 8>(src, pstride, n, nkp, Er, lsum);
+  else if (n <= 4 * bd) gather_parts<4, 4>(src, pstride, n, nkp, Er, lsum);
+  else gather_parts<8, 4>(src, pstride, n, nkp, Er, lsum);
   __syncthreads();
   if (a.logits)  // parity export: the fp32 logits the top-k below decides on
     for (int i = threadIdx.x; i < n; i += bd) a.logits[(size_t)t0 * Er + i] = lsum[i + i / Er];
   if (grp == 0) TG_STAMP_ANY(31);
+  if (cyc && threadIdx.x == 0) cyc[5] = clock64();
   // 256 threads = 32 tokens x 8; all lanes run every step (shuffles), writes are predicated
   const int r = threadIdx.x >> 3;
   const int per = (E + 7) / 8;
-  if (per <= 1) topk_rows<1>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else if (per <= 2) topk_rows<2>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else if (per <= 4) topk_rows<4>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else if (per <= 8) topk_rows<8>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else if (per <= 16) topk_rows<16>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
-  else topk_rows<32>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK);
+  if (per <= 1) topk_rows<1>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK, cyc);
+  else if (per <= 2) topk_rows<2>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK, cyc);
+  else if (per <= 4) topk_rows<4>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK, cyc);
+  else if (per <= 8) topk_rows<8>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK, cyc);
+  else if (per <= 16) topk_rows<16>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK, cyc);
+  else topk_rows<32>(a, rk, t0, r < nrow, lsum + r * ld, sl + r * kMaxK, cyc);
   if (grp == 0) TG_STAMP_ANY(37);
   __syncthreads();
   __syncthreads();
@@ -409,13 +488,19 @@ __device__ __forceinline__ void rank_chunk(const CallArgs &a, int chunk, uint8_t
   for (int i = tid; i < nkeys * 8; i += blockDim.x) bm[i] = 0;
   __syncthreads();
   int K[kMaxK];
-  for (int j = 0; j < k; ++j) {
-    K[j] = (t < a.T) ? __ldcg(a.key + (size_t)t * k + j) : -1;
-    if (K[j] >= 0) atomicOr(&bm[K[j] * 8 + (tid >> 5)], 1u << (tid & 31));
+  // every key load issued before the first use (clamped address, value dropped past T)
+  const int tc = min(t, max(a.T - 1, 0));
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) K[j] = (j < k) ? __ldcg(a.key + (size_t)tc * k + j) : -1;  // used below
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) {
+    if (t >= a.T) K[j] = -1;
+    if (j < k && K[j] >= 0) atomicOr(&bm[K[j] * 8 + (tid >> 5)], 1u << (tid & 31));
   }
   __syncthreads();
-  for (int j = 0; j < k; ++j) {
-    if (K[j] < 0) continue;
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) {  // (compile-time indices: K stays in registers)
+    if (j >= k || K[j] < 0) continue;
     const uint32_t *row = bm + K[j] * 8;
     int r = __popc(row[tid >> 5] & ((1u << (tid & 31)) - 1u));
     for (int wd = 0; wd < (tid >> 5); ++wd) r += __popc(row[wd]);
@@ -451,7 +536,7 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
     for (int b0 = 0; b0 < nchunks; b0 += 8) {  // 8 loads in flight (short code: this runs cold, once per call)
       int c[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = (b0 + u < nchunks) ? __ldcg(a.bcnt + (size_t)(b0 + u) * nkeys + K) : 0;
+      for (int u = 0; u < 8; ++u) c[u] = __ldcg(a.bcnt + (size_t)min(b0 + u, nchunks - 1) * nkeys + K);  // unconditional: all in flight
 #pragma unroll
       for (int u = 0; u < 8; ++u)
         if (b0 + u < nchunks) {
@@ -745,7 +830,15 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
         else cp_async_wait<0>();
         __syncthreads();
         if (it < 5) TG_STAMP(20 + 2 * it);
+        if (it == 1 && a.trace && threadIdx.x == 0 && VBID == 0) {  // effective SM clock of an item
+          a.trace[a.n_units_max + 148 + 64 + 1012] = globaltimer_ns();
+          a.trace[a.n_units_max + 148 + 64 + 1013] = clock64();
+        }
         router_compute(a, R, grp, kp, it % R.nbuf);
+        if (it == 1 && a.trace && threadIdx.x == 0 && VBID == 0) {
+          a.trace[a.n_units_max + 148 + 64 + 1014] = globaltimer_ns();
+          a.trace[a.n_units_max + 148 + 64 + 1015] = clock64();
+        }
         if (it < 5) TG_STAMP(21 + 2 * it);
         __syncthreads();  // buffer it % nbuf is free again
         if (it + R.nbuf < nit) router_issue(a, R, slot + (it + R.nbuf) * bpp, kp, it % R.nbuf, false);
@@ -754,13 +847,24 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     }
     // every CTA issues its share of the L2 prefetch, behind the router's own loads: the router
     // CTAs after their items (and their top-k chains), the idle ones after a short delay
+    if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + 552 + VBID] = globaltimer_ns();
     if (!(slot < bpp && slot < ngroups)) __nanosleep(2000);
-    l2_prefetch_share(a, bitem, VGRID);
+    // (decode-sized calls only: at prefill the front's own phases are slower beside it than the
+    // first weight tiles gain — same-box A/B, Qwen-shaped T = 8192: 789 / 811 µs without, 798 / 826 with)
+    if (chain) l2_prefetch_share(a, bitem, VGRID);
     post_wait_resets(a);
+    if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + 700 + VBID] = globaltimer_ns();
     if (!chain) {
       const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
       grid_barrier_z(gbar, nbar++, a.err, a.ncta);
-      for (int grp = VBID; grp < ngroups; grp += VGRID) group_topk(a, rk, grp, reinterpret_cast<float *>(R.tail));
+      if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + 848 + VBID] = globaltimer_ns();
+      for (int grp = VBID, i = 0; grp < ngroups; grp += VGRID, ++i) {
+        const long long c0 = clock64();
+        group_topk(a, rk, grp, reinterpret_cast<float *>(R.tail),
+                   (a.trace && VBID == 0 && i < 2) ? a.trace + a.n_units_max + 148 + 64 + 1000 + 6 * i : nullptr);
+        if (a.trace && threadIdx.x == 0 && i < 2)  // cycles of the block's first two groups (cold / warm code)
+          a.trace[a.n_units_max + 148 + 64 + 256 + 2 * VBID + i] = (uint64_t)(clock64() - c0);
+      }
       TG_STAMP(12);
       grid_barrier_z(gbar, nbar++, a.err, a.ncta);
       for (int ch = VBID; ch < nchunks; ch += VGRID) rank_chunk(a, ch, R.tail);

@@ -349,7 +349,13 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
       // stages get their A tiles at once and their token (B) tiles once every
       // source's rows have landed (release/acquire on per-source
       // epoch flags, then ordered before async-proxy reads).
-      bool data_ok = a.local_rows;  // world == 1: per-tile row counters instead (rdy)
+      // world > 1 without token dedup (NEXT-2, §6.1): a GEMM1 tile waits only for the
+      // data flags of the sources whose rows it holds (a slot's rows are ordered by source, so
+      // the all-gathered counts give each source's row range); dedup calls wait for every
+      // source (their dedup copies complete rows after the flags), replays likewise.
+      const bool per_src = !a.local_rows && !dedup && !a.replay;
+      bool data_ok = a.local_rows || per_src;  // world == 1: per-tile row counters instead (rdy)
+      const bool own_sh = a.Fsh > 0 && !a.replay && a.T > 0;  // shared-expert rows: own dispatch
       int npend = 0;  // pending token-tile loads, held by the lane that will issue them
       int pst[kStages], pkb[kStages], prow[kStages];
       uint32_t pab[kStages];
@@ -357,7 +363,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
       auto wait_data = [&]() {
         if (lane == 0) {
           for (int src = 0; src < a.world; ++src) {
-            if (__ldcg(a.need_src + src)) {
+            if (__ldcg(a.need_src + src) || (src == a.rank && own_sh)) {
               const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
                                    a.fslot_data * kMaxWorld + src;
               if (src == a.rank) {
@@ -387,8 +393,41 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
       // issued once the count is complete
       bool unit_ok = true;
       int udep = 0, urows = 0;
+      // per_src: sources whose data flag this producer holds, and the unit's sources
+      uint32_t have = 0, umask = 0;
+      const uint32_t part = per_src ? (uint32_t)__ldcg(a.sync + 6) : 0u;
+      const int32_t *cnt_all = reinterpret_cast<const int32_t *>(a.sym[a.rank] + a.L.cnt_all) +
+                               (size_t)a.cnt_buf * a.world * a.nkeys;
+      auto unit_sources = [&](const Unit &U) -> uint32_t {  // warp-uniform
+        if (U.kind == U_G1_SH) return 1u << a.rank;
+        const int K = a.rank * a.S_max + U.slot;
+        const int lo = U.n0 - S->rowoff[U.slot], hi = lo + U.nrows;
+        uint32_t m = 0;
+        int off = 0;
+        for (int q = 0; q < a.world && off < hi; ++q) {
+          if (!((part >> q) & 1u)) continue;  // failed in the count exchange: no rows
+          const int c = __ldcg(cnt_all + (size_t)q * a.nkeys + K);
+          if (c > 0 && off + c > lo) m |= 1u << q;
+          off += c;
+        }
+        return m;
+      };
       auto wait_rows = [&]() {
-        if (lane == 0) wait_ctr_ge(a.rdy + udep, urows, err, 0x4005);
+        if (per_src) {
+          if (lane == 0) {
+            for (int src = 0; src < a.world; ++src) {
+              if (!((umask >> src) & 1u) || ((have >> src) & 1u)) continue;
+              const uint32_t *fl = reinterpret_cast<const uint32_t *>(a.sym[a.rank] + a.L.flags) +
+                                   a.fslot_data * kMaxWorld + src;
+              if (src == a.rank) wait_flag_ge_s(fl, a.fepoch, sys, err, 0x4001);
+              else if (!wait_flag_or_fail(fl, a.fepoch, sys, a.fail_timeout_ns))
+                atomicOr(a.fail_mask, 1u << src);  // its rows never landed: computed on stale data, discarded
+            }
+          }
+          have |= umask;
+        } else if (lane == 0) {
+          wait_ctr_ge(a.rdy + udep, urows, err, 0x4005);
+        }
         __syncwarp();
         fence_proxy_async_global();
         unit_ok = true;
@@ -427,6 +466,9 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
           if (unit_ok) fence_proxy_async_global();
           udep = U.dep;
           urows = U.nrows;
+        } else if (g1 && per_src) {
+          umask = unit_sources(U);
+          unit_ok = (umask & ~have) == 0;  // flags acquired earlier: proxy fence already done
         }
         if (!g1) {
           if (!data_ok) wait_data();  // GEMM1 tiles waiting on pending B loads come first
@@ -633,7 +675,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
           // one origin lookup per token of the unit (not one per stored element: the loads would
           // serialise behind the stores they may alias), then a table read from smem
           for (int i = et; i < U.nrows; i += 128) {
-            const int2 o = meta[U.n0 + i];
+            const int2 o = __ldcg(meta + U.n0 + i);  // L2: this CTA may not hold the source's flag (NEXT-2)
             S->ydst[i] = reinterpret_cast<bf16 *>(a.sym[o.x] + a.L.ybuf) + (size_t)o.y * a.d;
           }
           named_bar_sync(1, 128);
@@ -690,7 +732,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
                   const bool v = n < U.nrows;
                   acc[i] = v ? __ldcg(reinterpret_cast<const float4 *>(a.ws + (size_t)(U.n0 + n) * a.d + c))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
-                  o[i] = v ? meta[U.n0 + n] : make_int2(0, 0);
+                  o[i] = v ? __ldcg(meta + U.n0 + n) : make_int2(0, 0);
                 }
                 for (int sp = 1; sp < U.nsplit; ++sp) {
                   float4 p[4];
@@ -737,7 +779,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
           for (int i = et; i < U.nrows; i += 128) {  // token tiles of up to 256 (wide mode)
             int src = a.rank, t = U.n0 - a.R_sh0 + i;
             if (!sh) {
-              const int2 o = meta[U.n0 + i];
+              const int2 o = __ldcg(meta + U.n0 + i);
               src = o.x;
               t = o.y / a.k;
             }

@@ -85,6 +85,7 @@ struct SymLayout {
 constexpr int FLAG_CNT = 0, FLAG_DATA = 1, FLAG_COMB = 2, FLAG_RDATA = 3, FLAG_RCOMB = 4, FLAG_RCNT = 5,
               kNumFlagKinds = 6;
 constexpr int kCntBufReplay = 2;  // cnt_all buffer of failover replays (calls use 0 / 1 by parity)
+constexpr long kTokCombMaxArrivals = 48 * 1024;  // world > 1: per-token combine up to this many NVLink arrivals per rank
 
 // Everything a call needs, by value (kernel parameter).
 struct CallArgs {

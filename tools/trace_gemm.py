@@ -56,8 +56,26 @@ def main():
         print("block0 items (start,end) us:", [(round((st[20 + 2 * i] - st[0]) / 1e3, 2), round((st[21 + 2 * i] - st[0]) / 1e3, 2)) for i in range(5) if st[20 + 2 * i]])
         fb = (tr["front_block_p1"] - st[0]) / 1e3
         print("front P1 finish per block: min %.1f median %.1f max %.1f  argmax %d" % (fb.min(), np.median(fb), fb.max(), int(np.argmax(fb))))
+        for key in ("front_block_router", "front_block_prefetch", "front_block_bar1"):
+            v = tr[key]
+            if (v > 0).any():
+                v = (v[v > 0] - st[0]) / 1e3
+                print("%s per block: min %.1f p10 %.1f median %.1f p90 %.1f max %.1f" % (
+                    key, v.min(), np.percentile(v, 10), np.median(v), np.percentile(v, 90), v.max()))
         tc = tr["topk_cycles"]
-        print("per-block gather/topk kcycles (cumulative over traced calls): max gather %.1f max topk %.1f, block of max topk %d" % (tc[:, 0].max() / 1e3, tc[:, 1].max() / 1e3, int(np.argmax(tc[:, 1]))))
+        if (tc[:, 1] > 0).any():  # grid-stride top-k: each block's first (cold code) and second group
+            c1, c2 = tc[:, 0][tc[:, 1] > 0], tc[:, 1][tc[:, 1] > 0]
+            print("top-k kcycles per group, block's first / second: median %.1f / %.1f, max %.1f / %.1f" % (
+                np.median(c1) / 1e3, np.median(c2) / 1e3, c1.max() / 1e3, c2.max() / 1e3))
+        ic = tr["item_clock"]
+        if ic[0] and ic[2] > ic[0]:
+            print("router item 1 of block 0: %.2f us, %d cycles -> %.0f MHz" % (
+                (ic[2] - ic[0]) / 1e3, ic[3] - ic[1], (ic[3] - ic[1]) / ((ic[2] - ic[0]) / 1e3)))
+        td = tr["topk_detail"].reshape(2, 6)
+        for i in range(2):
+            if td[i, 4]:
+                print("block 0 group %d top-k cycles: gather %d, select %d, slot+Z %d, stores %d" % (
+                    i, td[i, 5] - td[i, 4], td[i, 1] - td[i, 0], td[i, 2] - td[i, 1], td[i, 3] - td[i, 2]))
         if st[19] and st[18]:
             print("launch gap: previous call end -> entry %.2f us, entry -> front start (PDL wait) %.2f us"
                   % ((st[18] - st[19]) / 1e3, (st[0] - st[18]) / 1e3))
