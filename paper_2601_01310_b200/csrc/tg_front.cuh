@@ -647,6 +647,19 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
 // to kLocalLayoutBlock pairs (decode) it is run by the block that ran the count exchange, right
 // after it (no extra grid barrier); larger calls run it on every thread after the barrier.
 constexpr int kLocalLayoutBlock = 4096;
+
+// Early start (decode-sized single-rank calls): the GEMM phase begins without a grid barrier.
+// The chain's exchange block lays out the pairs, resets this call's counters (its buffer set was
+// last used by call n-2, which has exited once any CTA of call n runs: call n launched only after
+// every CTA of call n-1 triggered, each after its own front) and releases a per-set ready word
+// (sync[12] = epoch); a CTA waits for that word instead of for the last CTA of this call, which
+// starts only when the previous call's last CTA exits.  Under PDL the GEMM units of this call
+// thus run on the SMs the previous call's tail frees.  Row copies are then claimed dynamically
+// (sync[13]), so the CTAs that started first copy them.
+__device__ __forceinline__ bool early_start(const CallArgs &a) {
+  const int nkp = router_nkp(a.d, a.E_r), ngroups = (a.T + kRouterRows - 1) / kRouterRows;
+  return !a.replay && a.local_rows && a.T > 0 && ngroups <= (int)VGRID / nkp && a.T * a.k <= kLocalLayoutBlock;
+}
 __device__ __forceinline__ void local_layout(const CallArgs &a, int i0, int stride) {
   const int npairs = a.T * a.k;
   int2 *meta = reinterpret_cast<int2 *>(a.sym[a.rank] + a.L.meta);
@@ -666,6 +679,8 @@ __device__ __forceinline__ void local_layout(const CallArgs &a, int i0, int stri
 // the last chunk runs the count exchange (P3).  Arrival = __threadfence + atomic
 // counter (threadfence-reduction pattern); the last arriver resets the counter
 // for the next call (kernel boundaries order the calls).
+__device__ __forceinline__ void post_wait_resets(const CallArgs &a, int b, int nb_);
+
 __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, int nkp, int ngroups, float *sm) {
   __shared__ int s_last;
   if (threadIdx.x == 0) {
@@ -705,6 +720,14 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
   if (a.local_rows && a.T * a.k <= kLocalLayoutBlock) {
     __syncthreads();  // dbase, written by this block's exchange
     local_layout(a, threadIdx.x, blockDim.x);
+  }
+  if (early_start(a)) {
+    post_wait_resets(a, 0, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();  // layout, exchange outputs and resets before the ready word
+      atomicExch(a.sync + 12, (int)a.epoch);
+    }
   }
   __syncthreads();
 }
@@ -761,21 +784,23 @@ __device__ void l2_prefetch_share(const CallArgs &a, int part, int nparts) {
 
 // After griddepcontrol.wait (the previous launch has completed): reset what this launch's GEMM
 // phase counts on, and the counter set of the launch after next.
-__device__ __forceinline__ void post_wait_resets(const CallArgs &a) {
-  for (int i = VBID * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += VGRID * blockDim.x) a.ctr[i] = 0;
+__device__ __forceinline__ void post_wait_resets(const CallArgs &a, int b, int nb_) {
+  // (b, nb_): this block's index among the nb_ blocks sharing the resets
+  for (int i = b * blockDim.x + threadIdx.x; i < a.n_ctr_all; i += nb_ * blockDim.x) a.ctr[i] = 0;
   // this rank's per-token arrival counters: the peers add to them only after this rank's dispatch
   // (after the front's last grid barrier); the previous call's arrivals all landed before its combine
-  for (int i = VBID * blockDim.x + threadIdx.x; i < a.T; i += VGRID * blockDim.x) a.tokctr[i] = 0;
-  if (VBID == 0 && threadIdx.x == 0) a.sync[7] = 0;  // "combine incomplete" (a peer silent mid-call)
+  for (int i = b * blockDim.x + threadIdx.x; i < a.T; i += nb_ * blockDim.x) a.tokctr[i] = 0;
+  if (b == 0 && threadIdx.x == 0) a.sync[7] = 0;  // "combine incomplete" (a peer silent mid-call)
   const int nb = (a.cbuf + 2) % 3;
-  for (int i = VBID * blockDim.x + threadIdx.x; i < a.gmax; i += VGRID * blockDim.x) a.grp_ctr[(size_t)nb * a.gmax + i] = 0;
-  for (int i = VBID * blockDim.x + threadIdx.x; i < a.cmax; i += VGRID * blockDim.x) a.chunk_ctr[(size_t)nb * a.cmax + i] = 0;
-  if (VBID == 0 && threadIdx.x == 0) {
+  for (int i = b * blockDim.x + threadIdx.x; i < a.gmax; i += nb_ * blockDim.x) a.grp_ctr[(size_t)nb * a.gmax + i] = 0;
+  for (int i = b * blockDim.x + threadIdx.x; i < a.cmax; i += nb_ * blockDim.x) a.chunk_ctr[(size_t)nb * a.cmax + i] = 0;
+  if (b == 0 && threadIdx.x == 0) {
     *reinterpret_cast<unsigned long long *>(a.gsync + 8 + 4 * ((a.epoch + 1) & 1)) = 0ull;
     *reinterpret_cast<unsigned long long *>(a.sync + 10) = 0ull;  // the combine phase's barrier (replays)
     a.gsync[16 + nb] = 0;
   }
-  if (VBID == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
+  if (b == 0 && threadIdx.x < 5) a.sync[threadIdx.x] = 0;
+  if (b == 0 && threadIdx.x == 0) a.sync[13] = 0;  // row-copy claims (early-start calls)
 }
 
 // P1..P3 (all 256 threads of every CTA; cooperative grid).  Ends with a grid
@@ -816,7 +841,27 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     // rank phases between barriers (a chain would pile the top-k of many groups on the blocks
     // that happen to arrive last).
     const bool chain = ngroups <= bpp;
-    if (slot < bpp && slot < ngroups) {
+    const bool early = early_start(a);  // implies chain
+    if (early) {
+      // items claimed dynamically (numbered K-part-major: a block's successive items mostly
+      // share its staged Wg slice), so the CTAs that start first — on the SMs the previous call's
+      // tail frees first — run the whole router and its chain instead of waiting for the 64th CTA
+      const int nitems = ngroups * nkp;
+      int item = bitem, cur_kp = -1;
+      while (item < nitems) {
+        const int ikp = item / ngroups, grp = item % ngroups;
+        router_issue(a, R, grp, ikp, 0, ikp != cur_kp);
+        cur_kp = ikp;
+        if (threadIdx.x == 0) s_item = atomicAdd(a.gsync + 16 + a.cbuf, 1);  // the next one, meanwhile
+        cp_async_wait<0>();
+        __syncthreads();
+        const int next = s_item;
+        router_compute(a, R, grp, ikp, 0);
+        __syncthreads();
+        group_arrive(a, rk, grp, nkp, ngroups, reinterpret_cast<float *>(R.tail));
+        item = next;
+      }
+    } else if (slot < bpp && slot < ngroups) {
       const int nit = (ngroups - slot + bpp - 1) / bpp;
       const int pre = min(R.nbuf, nit);
       for (int i = 0; i < pre; ++i) router_issue(a, R, slot + i * bpp, kp, i, i == 0);
@@ -848,11 +893,11 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     // every CTA issues its share of the L2 prefetch, behind the router's own loads: the router
     // CTAs after their items (and their top-k chains), the idle ones after a short delay
     if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + 552 + VBID] = globaltimer_ns();
-    if (!(slot < bpp && slot < ngroups)) __nanosleep(2000);
+    if (early ? bitem >= ngroups * nkp : !(slot < bpp && slot < ngroups)) __nanosleep(2000);
     // (decode-sized calls only: at prefill the front's own phases are slower beside it than the
     // first weight tiles gain — same-box A/B, Qwen-shaped T = 8192: 789 / 811 µs without, 798 / 826 with)
-    if (chain) l2_prefetch_share(a, bitem, VGRID);
-    post_wait_resets(a);
+    if (chain) l2_prefetch_share(a, early ? VBID : bitem, VGRID);
+    if (!early) post_wait_resets(a, VBID, VGRID);  // (early start: the exchange block, before the ready word)
     if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + 700 + VBID] = globaltimer_ns();
     if (!chain) {
       const int nchunks = (a.T + kRankBlock - 1) / kRankBlock;
@@ -886,7 +931,12 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     }
   }
   if (a.trace && threadIdx.x == 0) a.trace[a.n_units_max + 148 + 64 + VBID] = globaltimer_ns();
-  grid_barrier_z(gbar, nbar++, a.err, a.ncta);
+  if (early_start(a)) {
+    if (threadIdx.x == 0) wait_ctr_ge(a.sync + 12, (int)a.epoch, a.err, 0x4006);
+    __syncthreads();
+  } else {
+    grid_barrier_z(gbar, nbar++, a.err, a.ncta);
+  }
   TG_STAMP(3);
   if (a.local_rows && a.T * a.k > kLocalLayoutBlock) {  // (smaller calls: by the exchange block)
     local_layout(a, VBID * blockDim.x + threadIdx.x, VGRID * blockDim.x);
@@ -906,7 +956,7 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
 __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys &rk, uint8_t *fsm) {
   unsigned long long *gbar = reinterpret_cast<unsigned long long *>(a.gsync + 8 + 4 * (a.epoch & 1));
   griddep_wait();
-  post_wait_resets(a);
+  post_wait_resets(a, VBID, VGRID);
   int nbar = 0;
   const int npairs = a.T * a.k;
   for (int p = VBID * blockDim.x + threadIdx.x; p < npairs; p += VGRID * blockDim.x) {
@@ -989,11 +1039,12 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) 
 // = the order the GEMM work list consumes the tiles, so the first units start after a few
 // rows, not after the whole dispatch.  grp_of(r, shared) -> token-tile group of a row.
 template <typename GroupOf>
-__device__ __forceinline__ void dispatch_local_rows(const CallArgs &a, int w, int nw, int nrecv, GroupOf grp_of) {
+__device__ __forceinline__ void dispatch_local_rows(const CallArgs &a, int w, int nw, int nrecv, GroupOf grp_of,
+                                                    int *claim = nullptr) {
   const int lane = threadIdx.x & 31, nch = a.d >> 3;
   const int nsh = (a.Fsh > 0) ? a.T : 0;
   uint4 *recv = reinterpret_cast<uint4 *>(a.sym[a.rank] + a.L.recv);
-  for (int r = w; r < nrecv + nsh; r += nw) {
+  auto copy_one = [&](int r) {
     const bool sh = r >= nrecv;
     const int row = sh ? a.R_sh0 + (r - nrecv) : r;
     const int t = sh ? r - nrecv : __ldcg(a.srcrow + r);
@@ -1004,6 +1055,19 @@ __device__ __forceinline__ void dispatch_local_rows(const CallArgs &a, int w, in
       __threadfence();
       atomicAdd(a.rdy + grp_of(sh ? r - nrecv : r, sh), 1);
     }
+  };
+  const int total = nrecv + nsh;
+  if (claim) {  // early start: rows claimed in receive order by whichever warps run first
+    constexpr int kClaim = 4;
+    for (;;) {
+      int r0 = 0;
+      if (lane == 0) r0 = atomicAdd(claim, kClaim);
+      r0 = __shfl_sync(0xffffffffu, r0, 0);
+      if (r0 >= total) break;
+      for (int r = r0; r < min(r0 + kClaim, total); ++r) copy_one(r);
+    }
+  } else {
+    for (int r = w; r < total; r += nw) copy_one(r);
   }
 }
 

@@ -591,7 +591,7 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
         if (shr) return S->goff[a.S_loc] + r / a.bn;
         const int s = find_seg(S->rowoff, a.S_loc, r);
         return S->goff[s] + (r - S->rowoff[s]) / a.bn;
-      });
+      }, early_start(a) ? a.sync + 13 : nullptr);
     }
     // ===================== token dedup, receiving side (warps 2-7, multi-GPU) =====================
     if (dedup) {
