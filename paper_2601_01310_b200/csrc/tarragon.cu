@@ -257,9 +257,12 @@ tg_status tg_init(const tg_config *cfg, int rank, int world, int cuda_device, tg
   c->R_cap = world * c->T_max * std::min(k, std::max(c->S_max, 1));
   c->R_sh0 = c->R_cap;
   c->R_tot = c->R_cap + (Fsh > 0 ? c->T_max : 0);
-  // fixed split-K for long GEMM2 reductions: a function of the shape only
-  // (r02 same-box A/B at Mixtral decode, F = 14336: 1 split 500.6 us, 2 splits 494.8, 4 splits 508.5:
-  // the fp32 partials cost HBM traffic, one split leaves 140-us units for the last wave)
+  // fixed split-K for long GEMM2 reductions: a function of the shape only, so outputs are bitwise
+  // equal at every GPU count (P7).  Same-box A/B at Mixtral decode, F = 14336, us per call, 2 vs 4
+  // splits, with early start: 1 GPU 475.3 vs 482.8, 2 GPUs 257.6 vs 265.6, 4 GPUs 161.4 vs 165.4
+  // (before early start at world > 1, 4 splits won there — 4 GPUs 207.4 vs 189.8 — as the last
+  // GEMM2 wave of a rank serving 2 experts idled most SMs; now the next call's GEMM fills that
+  // tail).  1 split leaves 140-us units for the last wave.
   c->nsplit = (F / BK >= 128 && (F / BK) % 2 == 0) ? 2 : 1;
   if (const char *ns = getenv("TG_NSPLIT")) {  // development override (A/B timing)
     const int v = atoi(ns);

@@ -658,7 +658,12 @@ constexpr int kLocalLayoutBlock = 4096;
 // (sync[13]), so the CTAs that started first copy them.
 __device__ __forceinline__ bool early_start(const CallArgs &a) {
   const int nkp = router_nkp(a.d, a.E_r), ngroups = (a.T + kRouterRows - 1) / kRouterRows;
-  return !a.replay && a.local_rows && a.T > 0 && ngroups <= (int)VGRID / nkp && a.T * a.k <= kLocalLayoutBlock;
+  if (a.replay || a.T <= 0 || ngroups > (int)VGRID / nkp) return false;
+  if (a.local_rows) return a.T * a.k <= kLocalLayoutBlock;
+  // world > 1: the pairs are dispatched by claims after the ready word (the data flags released
+  // by the warp completing the last pair); never with token dedup, whose copies wait for every
+  // CTA (dedup needs >= 16 MB of rows, an upper bound of which is static)
+  return (long long)a.T_max * a.world * a.k * a.d * 2 < (16ll << 20);
 }
 __device__ __forceinline__ void local_layout(const CallArgs &a, int i0, int stride) {
   const int npairs = a.T * a.k;
@@ -979,22 +984,24 @@ __device__ __forceinline__ void replay_front(const CallArgs &a, const RouteKeys 
 // P4 dispatch on `nw` warps (this one is warp `w`, grid-wide numbering): one warp
 // per (token, j) pair, then the shared-expert rows.  The caller syncs its
 // dispatch warps and calls dispatch_done() from one thread.
-__device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) {
+__device__ __forceinline__ void release_data_flags(const CallArgs &a);
+
+__device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw, int *claim = nullptr) {
   const int lane = threadIdx.x & 31;
   const int k = a.k, nch = a.d >> 3;
   const int npairs = a.T * k;
   const int nsh = (a.Fsh > 0 && !a.replay) ? a.T : 0;  // a replay keeps the shared expert's output
   const bool dedup = __ldcg(a.sync + 5) != 0;
   const uint32_t part = (uint32_t)__ldcg(a.sync + 6);  // ranks taking part in this run
-  for (int p = w; p < npairs + nsh; p += nw) {
+  auto one = [&](int p) {
     if (p < npairs) {
       const int t = p / k;
       const int K = __ldcg(a.key + p);
-      if (K < 0) continue;  // failover replay: pair not recomputed
+      if (K < 0) return;  // failover replay: pair not recomputed
       const int q = K / a.S_max;
       if (!((part >> q) & 1u)) {  // destination failed in the count exchange: re-routed by tg_failover
         if (lane == 0) a.dst_pos[p] = -1;
-        continue;
+        return;
       }
       const int pos =
           __ldcg(a.dbase + K) + __ldcg(a.bcnt + (size_t)(t / kRankBlock) * a.nkeys + K) + __ldcg(a.lrank + p);
@@ -1028,6 +1035,27 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw) 
       const uint4 *src = reinterpret_cast<const uint4 *>(a.x + (size_t)t * a.d);
       uint4 *dst = reinterpret_cast<uint4 *>(a.sym[a.rank] + a.L.recv) + (size_t)(a.R_sh0 + t) * nch;
       copy_row(dst, src, nch, lane);
+    }
+  };
+  const int total = npairs + nsh;
+  if (!claim) {
+    for (int p = w; p < total; p += nw) one(p);
+    return;
+  }
+  // early start: pairs claimed by whichever warps run first; the warp that completes the last
+  // pair releases the data flags (sync[3] counts completed pairs)
+  constexpr int kClaim = 4;
+  for (;;) {
+    int p0 = 0;
+    if (lane == 0) p0 = atomicAdd(claim, kClaim);
+    p0 = __shfl_sync(0xffffffffu, p0, 0);
+    if (p0 >= total) break;
+    const int p1 = min(p0 + kClaim, total);
+    for (int p = p0; p < p1; ++p) one(p);
+    __syncwarp();
+    if (lane == 0) {
+      fence_scope(a.world > 1);  // this warp's row / origin stores (peer memory) before the count
+      if (atomicAdd(a.sync + 3, p1 - p0) + (p1 - p0) == total) release_data_flags(a);
     }
   }
 }
@@ -1087,10 +1115,8 @@ __device__ __forceinline__ void dedup_copies(const CallArgs &a, int w, int nw, i
 
 // Data-ready flags: the last CTA to finish its dispatch releases one flag per
 // live destination (one thread per CTA, after its dispatch warps synced).
-__device__ __forceinline__ void dispatch_done(const CallArgs &a) {
+__device__ __forceinline__ void release_data_flags(const CallArgs &a) {
   const bool sys = a.world > 1;
-  fence_scope(sys);
-  if (atomicAdd(&a.sync[3], 1) != (int)VGRID - 1) return;
   fence_scope(sys);
   const uint32_t part = (uint32_t)__ldcg(a.sync + 6);
   for (int q = 0; q < a.world; ++q) {
@@ -1099,6 +1125,12 @@ __device__ __forceinline__ void dispatch_done(const CallArgs &a) {
     st_release(fl, a.fepoch, sys);
   }
   if (a.trace) a.trace[a.n_units_max + 148 + 4] = globaltimer_ns();
+}
+
+__device__ __forceinline__ void dispatch_done(const CallArgs &a) {
+  fence_scope(a.world > 1);
+  if (atomicAdd(&a.sync[3], 1) != (int)VGRID - 1) return;
+  release_data_flags(a);
 }
 
 __host__ __device__ inline size_t tg_max(size_t x, size_t y) { return x > y ? x : y; }

@@ -290,9 +290,13 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
   // ===================== P4 dispatch (all warps; r01 A/B: 3.5% faster at 4 GPUs than on
   // warps 2-7 beside the first weight loads, equal at 1 GPU) =====================
   if (!a.local_rows) {
-    dispatch_rows(a, VBID * 8 + (threadIdx.x >> 5), VGRID * 8);
-    __syncthreads();
-    if (threadIdx.x == 0) dispatch_done(a);
+    if (early_start(a)) {
+      dispatch_rows(a, 0, 0, a.sync + 13);  // claims; the data flags go out with the last pair
+    } else {
+      dispatch_rows(a, VBID * 8 + (threadIdx.x >> 5), VGRID * 8);
+      __syncthreads();
+      if (threadIdx.x == 0) dispatch_done(a);
+    }
   }
   if (a.inject_fail) return;  // fault injection (tests): crash after the dispatch, the peers hold the rows
   // the next call may start now (PDL): its front runs on the SMs this call's tail frees, and waits
