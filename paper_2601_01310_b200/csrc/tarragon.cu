@@ -764,6 +764,8 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
     // arrivals and the sources' waits must take the same branch.
     const long arrivals = (long)c->T_max * c->k * ((c->d + 2 * BM - 1) / (2 * BM));
     a.tok_comb = comb && (c->world == 1 || arrivals <= kTokCombMaxArrivals) ? 1 : 0;
+    const char *lb = getenv("TG_LAYOUT");  // development override (A/B timing)
+    a.layout_block = lb ? atoi(lb) : kLocalLayoutBlock;
     const char *dv = getenv("TG_DEV");
     a.dev = dv ? atoi(dv) : 0;
   }

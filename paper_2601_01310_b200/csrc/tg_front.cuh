@@ -646,7 +646,6 @@ __device__ __forceinline__ void exchange_counts(const CallArgs &a, int nchunks, 
 // row (the rows themselves are copied in row order beside the GEMM, dispatch_local_rows).  Up
 // to kLocalLayoutBlock pairs (decode) it is run by the block that ran the count exchange, right
 // after it (no extra grid barrier); larger calls run it on every thread after the barrier.
-constexpr int kLocalLayoutBlock = 4096;
 
 // Early start (decode-sized single-rank calls): the GEMM phase begins without a grid barrier.
 // The chain's exchange block lays out the pairs, resets this call's counters (its buffer set was
@@ -659,7 +658,7 @@ constexpr int kLocalLayoutBlock = 4096;
 __device__ __forceinline__ bool early_start(const CallArgs &a) {
   const int nkp = router_nkp(a.d, a.E_r), ngroups = (a.T + kRouterRows - 1) / kRouterRows;
   if (a.replay || a.T <= 0 || ngroups > (int)VGRID / nkp) return false;
-  if (a.local_rows) return a.T * a.k <= kLocalLayoutBlock;
+  if (a.local_rows) return a.T * a.k <= a.layout_block;
   // world > 1: the pairs are dispatched by claims after the ready word (the data flags released
   // by the warp completing the last pair); never with token dedup, whose copies wait for every
   // CTA (dedup needs >= 16 MB of rows, an upper bound of which is static)
@@ -722,7 +721,7 @@ __device__ void group_arrive(const CallArgs &a, const RouteKeys &rk, int grp, in
   TG_STAMP_ANY(1);
   exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(sm));
   TG_STAMP_ANY(14);
-  if (a.local_rows && a.T * a.k <= kLocalLayoutBlock) {
+  if (a.local_rows && a.T * a.k <= a.layout_block) {
     __syncthreads();  // dbase, written by this block's exchange
     local_layout(a, threadIdx.x, blockDim.x);
   }
@@ -924,7 +923,7 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
         TG_STAMP(1);
         exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(R.tail));
         TG_STAMP(14);
-        if (a.local_rows && a.T * a.k <= kLocalLayoutBlock) {
+        if (a.local_rows && a.T * a.k <= a.layout_block) {
           __syncthreads();
           local_layout(a, threadIdx.x, blockDim.x);
         }
@@ -943,7 +942,7 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     grid_barrier_z(gbar, nbar++, a.err, a.ncta);
   }
   TG_STAMP(3);
-  if (a.local_rows && a.T * a.k > kLocalLayoutBlock) {  // (smaller calls: by the exchange block)
+  if (a.local_rows && a.T * a.k > a.layout_block) {  // (smaller calls: by the exchange block)
     local_layout(a, VBID * blockDim.x + threadIdx.x, VGRID * blockDim.x);
     grid_barrier_z(gbar, nbar++, a.err, a.ncta);
   }

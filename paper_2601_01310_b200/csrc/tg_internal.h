@@ -85,6 +85,7 @@ struct SymLayout {
 constexpr int FLAG_CNT = 0, FLAG_DATA = 1, FLAG_COMB = 2, FLAG_RDATA = 3, FLAG_RCOMB = 4, FLAG_RCNT = 5,
               kNumFlagKinds = 6;
 constexpr int kCntBufReplay = 2;  // cnt_all buffer of failover replays (calls use 0 / 1 by parity)
+constexpr int kLocalLayoutBlock = 4096;  // world == 1: default of CallArgs::layout_block
 constexpr long kTokCombMaxArrivals = 48 * 1024;  // world > 1: per-token combine up to this many NVLink arrivals per rank
 
 // Everything a call needs, by value (kernel parameter).
@@ -153,6 +154,7 @@ struct CallArgs {
   int n_ctr_all;         // ctr + rdy entries (reset together at the start of a call)
   int32_t *srcrow;       // [R_cap] world == 1: token of each received row
   int local_rows;        // world == 1: rows copied in row order beside the GEMM, per-tile counters
+  int layout_block;      // world == 1: pairs up to which the exchange block lays out the call (decode)
   int tok_comb;          // per-token arrival counters, combine without a grid barrier (not in replays)
   int dev;               // development A/B switches (TG_DEV)
   int cta0, ncta;        // this rank's CTAs in the launch: [cta0, cta0 + ncta) (several virtual ranks
