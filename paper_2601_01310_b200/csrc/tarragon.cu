@@ -42,6 +42,15 @@ PFN_encodeTiled get_encode() {
   return fn;
 }
 
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_streamValue32 get_stream_op(const char *name) {
+  void *p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<PFN_streamValue32>(p);
+  return nullptr;
+}
+
 }  // namespace
 
 struct tg_ctx {
@@ -102,6 +111,9 @@ struct tg_ctx {
   cudaStream_t hs_h2d = nullptr, hs_d2h = nullptr;  // host-path copy streams (overlap with the layer)
   cudaEvent_t ev_h2d[2] = {}, ev_k[2] = {}, ev_d2h[2] = {}, ev_sync = nullptr, ev_sync2 = nullptr;
   long long host_calls = 0;
+  int *hk_dev = nullptr;                          // host-path device words (CallArgs::hk)
+  PFN_streamValue32 wait32 = nullptr, write32 = nullptr;
+  bool pend_host = false;                         // the next launch is host call host_calls
   uint32_t epoch = 0;    // local kernel runs
   uint32_t xepoch = 0;   // calls (equal on every rank)
   uint32_t rxepoch = 0;  // failover replays (equal on every surviving rank)
@@ -770,6 +782,13 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
     a.dev = dv ? atoi(dv) : 0;
   }
   a.alive = c->alive;
+  a.hk = nullptr;
+  if (c->pend_host) {
+    a.hk = c->hk_dev;
+    a.hcall = (int)(c->host_calls + 1);
+    a.hb = (int)(c->host_calls & 1);
+    a.hexit = (int)((c->host_calls / 2 + 1) * (long long)c->n_sms - 1);  // grid = n_sms CTAs
+  }
   a.fslot_data = FLAG_DATA;
   a.fslot_comb = FLAG_COMB;
   a.fslot_cnt = FLAG_CNT;
@@ -1028,6 +1047,12 @@ static tg_status host_path_init(tg_ctx *c) {
   }
   CK(cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_sync2, cudaEventDisableTiming));
+  c->wait32 = get_stream_op("cuStreamWaitValue32");
+  c->write32 = get_stream_op("cuStreamWriteValue32");
+  if (c->wait32 && c->write32) {
+    CK(cudaMalloc(&c->hk_dev, 8 * sizeof(int)));
+    CK(cudaMemset(c->hk_dev, 0, 8 * sizeof(int)));
+  }
   return TG_OK;
 }
 
@@ -1043,6 +1068,34 @@ tg_status tg_moe_layer_host(tg_ctx *c, const void *xh, void *oh, int T, void *st
   if (st) return st;
   const int b = (int)(c->host_calls & 1);
   const size_t bytes = (size_t)T * c->d * 2;
+  if (c->hk_dev) {
+    // no stream op between consecutive kernels on `stream` (that would serialise them: PDL):
+    // the copy streams wait on / write device words, the kernel polls them (CallArgs::hk)
+    const int hcall = (int)(c->host_calls + 1);
+    CUstream h2d = reinterpret_cast<CUstream>(c->hs_h2d), d2h = reinterpret_cast<CUstream>(c->hs_d2h);
+    const CUdeviceptr w = reinterpret_cast<CUdeviceptr>(c->hk_dev);
+    if (c->host_calls < 2) {  // first uses of the buffers: after the work already on `stream`
+      CK(cudaEventRecord(c->ev_sync, s));
+      CK(cudaStreamWaitEvent(c->hs_h2d, c->ev_sync, 0));
+    } else if (c->wait32(h2d, w + (6 + b) * 4, (cuuint32_t)(hcall - 2), CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+      return fail(c, TG_ERR_CUDA, "cuStreamWaitValue32 failed");  // x_stage[b] free once call i-2 completed
+    }
+    if (T > 0) CK(cudaMemcpyAsync(c->x_stage[b], xh, bytes, cudaMemcpyHostToDevice, c->hs_h2d));
+    if (c->write32(h2d, w + (0 + b) * 4, (cuuint32_t)hcall, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return fail(c, TG_ERR_CUDA, "cuStreamWriteValue32 failed");
+    c->pend_host = true;
+    st = tg_moe_layer(c, c->x_stage[b], c->out_stage[b], T, stream);
+    c->pend_host = false;
+    if (st) return st;
+    if (c->wait32(d2h, w + (6 + b) * 4, (cuuint32_t)hcall, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return fail(c, TG_ERR_CUDA, "cuStreamWaitValue32 failed");
+    if (T > 0) CK(cudaMemcpyAsync(oh, c->out_stage[b], bytes, cudaMemcpyDeviceToHost, c->hs_d2h));
+    if (c->write32(d2h, w + (2 + b) * 4, (cuuint32_t)hcall, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return fail(c, TG_ERR_CUDA, "cuStreamWriteValue32 failed");
+    ++c->host_calls;
+    return TG_OK;
+  }
+  // (no stream memory operations: event ordering, which serialises consecutive layer launches)
   if (c->host_calls < 2) {  // first uses of the buffers: ordered after the work already on `stream`
     CK(cudaEventRecord(c->ev_sync, s));
     CK(cudaStreamWaitEvent(c->hs_h2d, c->ev_sync, 0));

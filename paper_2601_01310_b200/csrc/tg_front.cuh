@@ -852,6 +852,35 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
       // tail frees first — run the whole router and its chain instead of waiting for the 64th CTA
       const int nitems = ngroups * nkp;
       int item = bitem, cur_kp = -1;
+      if (a.E_r <= 32 && R.nbuf >= 2) {
+        // two Wg slices fit the slice region (rows [0, 32) and [32, 64)): the next item is claimed
+        // and its loads issued before this one computes
+        auto half = [&](int b) {
+          RouterSmem Rb = R;
+          Rb.wg = R.wg + (size_t)b * 32 * R.ldw;
+          return Rb;
+        };
+        int b = 0;
+        if (item < nitems) router_issue(a, half(0), item % ngroups, item / ngroups, 0, true);
+        while (item < nitems) {
+          if (threadIdx.x == 0) s_item = atomicAdd(a.gsync + 16 + a.cbuf, 1);
+          __syncthreads();
+          const int next = s_item;
+          if (next < nitems) {
+            router_issue(a, half(b ^ 1), next % ngroups, next / ngroups, b ^ 1, true);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          __syncthreads();
+          const int grp = item % ngroups;
+          router_compute(a, half(b), grp, item / ngroups, b);
+          __syncthreads();
+          group_arrive(a, rk, grp, nkp, ngroups, reinterpret_cast<float *>(R.tail));
+          item = next;
+          b ^= 1;
+        }
+      }
       while (item < nitems) {
         const int ikp = item / ngroups, grp = item % ngroups;
         router_issue(a, R, grp, ikp, 0, ikp != cur_kp);

@@ -284,6 +284,10 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
     a.trace[a.n_units_max + 148 + 18] = globaltimer_ns();
   }
   // PDL: this call may run beside the previous one's tail (its buffer set is the other one)
+  if (a.hk) {  // host-buffer path: x staged by the H2D copy stream (CallArgs::hk)
+    if (threadIdx.x == 0) wait_ctr_ge(a.hk + a.hb, a.hcall, a.err, 0x4007);
+    __syncthreads();
+  }
   // ===================== front: P1 router .. P3 count exchange (tg_front.cuh) =====================
   if (a.replay) replay_front(a, rk, smem_raw);
   else front_phase(a, rk, smem_raw);
@@ -809,6 +813,10 @@ __device__ __forceinline__ void layer_body(const TmaMaps &maps, const CallArgs &
   }
 
   // ===================== combine (GK5), all CTAs =====================
+  if (a.hk && a.hcall > 2) {  // host-buffer path: out_stage drained by call i-2's D2H copy
+    if (threadIdx.x == 0) wait_ctr_ge(a.hk + 2 + a.hb, a.hcall - 2, err, 0x4008);
+    __syncthreads();
+  }
   if (a.tok_comb) {
     const uint32_t part = (uint32_t)__ldcg(a.sync + 6);
     if (a.world > 1) {
@@ -900,6 +908,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_layer(const __grid_constant__ TmaMaps maps, const __grid_constant__ CallArgs a,
             const __grid_constant__ RouteKeys rk) {
   layer_body(maps, a, rk);
+  if (a.hk) {  // host-buffer path: the last CTA to exit marks the call complete (D2H, next H2D)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(a.hk + 4 + a.hb, 1) == a.hexit) {
+        __threadfence();
+        atomicExch(a.hk + 6 + a.hb, a.hcall);
+      }
+    }
+  }
 }
 
 // Virtual ranks of one GPU as ONE cooperative launch (tests; a GPU shared by several AW/EW

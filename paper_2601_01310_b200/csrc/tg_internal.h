@@ -156,6 +156,12 @@ struct CallArgs {
   int local_rows;        // world == 1: rows copied in row order beside the GEMM, per-tile counters
   int layout_block;      // world == 1: pairs up to which the exchange block lays out the call (decode)
   int tok_comb;          // per-token arrival counters, combine without a grid barrier (not in replays)
+  // host-buffer path (tg_moe_layer_host): device words shared with the copy streams, which order
+  // themselves with stream memory operations so no stream op sits between consecutive kernels
+  // (the PDL overlap); null otherwise.  [0,1] x staged, [2,3] out drained, [4,5] exit counts,
+  // [6,7] call complete — per staging buffer hb; values are host call numbers hcall (1-based)
+  int *hk;
+  int hcall, hb, hexit;
   int dev;               // development A/B switches (TG_DEV)
   int cta0, ncta;        // this rank's CTAs in the launch: [cta0, cta0 + ncta) (several virtual ranks
                          // of one GPU share one cooperative launch: tg_moe_layer_multi)

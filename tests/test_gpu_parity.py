@@ -199,9 +199,13 @@ def test_empty_call_and_errors():
     assert torch.equal(out.view(torch.int16), o2.view(torch.int16))
 
 
-def test_host_entry_point_e2e():
-    """tg_moe_layer_host: pinned host in/out, copies inside the call."""
-    tg, sh, L, x, pl, layer = _setup("tiny", 2, seed=1005)
+@pytest.mark.parametrize("cfg,ncalls", [("tiny", 12), ("mixtral_decode", 8)])
+def test_host_entry_point_e2e(cfg, ncalls):
+    """tg_moe_layer_host: pinned host in/out, copies inside the call; the copy streams are
+    ordered against the layer launches by device words (no stream op between the launches), over
+    the two staging buffers, with a different token count per call."""
+    tg, sh, L, x, pl, layer = _setup(cfg, 2, seed=1005)
+    layer.export_stages(False)  # nothing else on the stream between the launches
     xh = x.pin_memory()
     oh = torch.empty_like(xh).pin_memory()
     assert tg.tg_moe_layer_host(layer.ctx, xh, oh) == tg.TG_OK
@@ -209,8 +213,9 @@ def test_host_entry_point_e2e():
     torch.cuda.synchronize()
     od = _run(layer, x)
     assert torch.equal(oh.view(torch.int16), od.cpu().view(torch.int16))
-    # pipelined calls over the two staging buffers, different inputs per call
-    xs = [wl.make_tokens(sh, 2000 + i).pin_memory() for i in range(5)]
+    # pipelined calls over the two staging buffers, different inputs (and sizes) per call
+    sizes = [sh.T, max(sh.T - 3, 1), max(sh.T // 2, 1), 1, sh.T]
+    xs = [wl.make_tokens(sh, 2000 + i, sizes[i % len(sizes)]).pin_memory() for i in range(ncalls)]
     ohs = [torch.empty_like(v).pin_memory() for v in xs]
     for v, o in zip(xs, ohs):
         assert tg.tg_moe_layer_host(layer.ctx, v, o) == tg.TG_OK
