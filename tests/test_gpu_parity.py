@@ -274,3 +274,32 @@ def test_next3b_gating_variants(cfg, W):
     """NEXT-3b: the public DS-V2-Lite / Qwen1.5-MoE gating (softmax over all E, top-k weights not
     renormalised) and Qwen's sigmoid-gated shared expert (F_sh 5632), parity + mask bit-identity."""
     _big(cfg, 2005, n_sample=32, W=W)
+
+
+@pytest.mark.parametrize("cfg,ncalls", [("mixtral_decode", 240), ("ds_v2_lite_decode", 160), ("qwen_prefill", 40)])
+def test_back_to_back_calls(cfg, ncalls):
+    """Epoch-flag / buffer-set stress: ncalls launches back to back with no host
+    synchronisation — consecutive calls overlap (PDL), decode calls start their GEMM on a ready
+    word with claimed router items and row copies — alternating two inputs and, on the host-buffer
+    path, ordered by device words; every output is bitwise the single call's output for its input."""
+    tg, sh, L, x0, pl, layer = _setup(cfg, 2, seed=1100)
+    layer.export_stages(False)
+    xs = [x0.cuda(), wl.make_tokens(sh, 1101).cuda()]
+    refs = [_run(layer, v).clone() for v in xs]
+    outs = [torch.empty_like(xs[0]) for _ in range(ncalls)]
+    for i in range(ncalls):
+        layer(xs[i % 2], outs[i])
+    torch.cuda.synchronize()
+    bad = [i for i in range(ncalls) if not torch.equal(outs[i].view(torch.int16), refs[i % 2].view(torch.int16))]
+    assert not bad, f"calls {bad[:8]} (of {len(bad)}) differ from their input's reference"
+    # host-buffer path, same stress
+    xh = [v.cpu().pin_memory() for v in xs]
+    n_h = min(ncalls, 64) if sh.T <= 1024 else 8  # (pinned host memory)
+    ohs = [torch.empty_like(xh[0]).pin_memory() for _ in range(n_h)]
+    for i in range(n_h):
+        assert tg.tg_moe_layer_host(layer.ctx, xh[i % 2], ohs[i]) == tg.TG_OK
+    tg.tg_host_sync(layer.ctx)
+    torch.cuda.synchronize()
+    bad = [i for i in range(n_h) if not torch.equal(ohs[i].view(torch.int16), refs[i % 2].cpu().view(torch.int16))]
+    assert not bad, f"host-path calls {bad[:8]} (of {len(bad)}) differ"
+    layer.close()
