@@ -250,7 +250,12 @@ tg_status tg_moe_layer(tg_ctx *ctx, const void *x, void *out, int n_tokens, void
  * calls on `stream`.  The outputs (and the right to reuse x_host) are
  * guaranteed once `stream` passes a later tg_host_sync(ctx, stream), which
  * makes `stream` wait for every pending host-path copy and orders the next
- * host-path copies after the work already on `stream`.                     */
+ * host-path copies after the work already on `stream`.  The copy streams are
+ * ordered against the layer launches by device words (cuStreamWaitValue32 /
+ * cuStreamWriteValue32 on the copy streams, polled by the kernel), so nothing
+ * is enqueued on `stream` between two consecutive layer launches and they
+ * overlap as tg_moe_layer calls do; where stream memory operations are not
+ * available, event ordering is used instead (the launches then serialise).  */
 tg_status tg_host_sync(tg_ctx *ctx, void *stream);
 tg_status tg_moe_layer_host(tg_ctx *ctx, const void *x_host, void *out_host, int n_tokens,
                             void *stream);
