@@ -807,6 +807,66 @@ __device__ __forceinline__ void post_wait_resets(const CallArgs &a, int b, int n
   if (b == 0 && threadIdx.x == 0) a.sync[13] = 0;  // row-copy claims (early-start calls)
 }
 
+// World == 1, prefill-sized calls: P3 and the pair layout without a serial exchange block.
+// After the rank phase every block derives, in shared memory, the per-key exclusive chunk bases
+// and slot offsets from the chunk counts (the same scans exchange_counts runs at world == 1 —
+// there are no peers to gather from) and lays out its grid-stride share of the pairs; block 0
+// also writes what the GEMM phase and the exports read.  base: [nchunks][nkeys], tot / dofs:
+// [nkeys] ints of shared memory.
+__device__ __forceinline__ void local_exchange_layout(const CallArgs &a, int nchunks, int32_t *base, int32_t *tot,
+                                                      int32_t *dofs) {
+  const int tid = threadIdx.x, bd = blockDim.x, nkeys = a.nkeys, k0 = a.rank * a.S_max;
+  for (int K = tid; K < nkeys; K += bd) {
+    int run = 0;
+    for (int b0 = 0; b0 < nchunks; b0 += 8) {
+      int c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] = __ldcg(a.bcnt + (size_t)min(b0 + u, nchunks - 1) * nkeys + K);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b0 + u < nchunks) {
+          base[(b0 + u) * nkeys + K] = run;
+          run += c[u];
+        }
+    }
+    tot[K] = run;
+  }
+  __syncthreads();
+  for (int K = tid; K < nkeys; K += bd) {
+    const int sl = K - k0;
+    int off = 0;
+    if (sl >= 0 && sl < a.S_max)
+      for (int s2 = 0; s2 < sl; ++s2) off += tot[k0 + s2];
+    dofs[K] = off;
+  }
+  __syncthreads();
+  if (VBID == 0) {
+    for (int K = tid; K < nkeys; K += bd) {
+      a.gcounts[K] = tot[K];
+      a.dbase[K] = dofs[K];
+      atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + K), (unsigned long long)tot[K]);
+    }
+    for (int sl = tid; sl < a.S_loc; sl += bd) a.slot_rows[sl] = tot[k0 + sl];
+    if (tid == 0) {
+      int any = 0;
+      for (int sl = 0; sl < a.S_max; ++sl) any |= tot[k0 + sl];
+      a.need_src[a.rank] = any > 0;
+      a.sent_to[a.rank] = any > 0;
+      a.sync[5] = 0;  // no token dedup without peers
+      a.sync[6] = (int)(1u << a.rank);
+    }
+  }
+  int2 *meta = reinterpret_cast<int2 *>(a.sym[a.rank] + a.L.meta);
+  const int npairs = a.T * a.k;
+  for (int p = VBID * bd + tid; p < npairs; p += VGRID * bd) {
+    const int t = p / a.k, K = __ldcg(a.key + p);
+    const int pos = dofs[K] + base[(t / kRankBlock) * nkeys + K] + __ldcg(a.lrank + p);
+    a.dst_pos[p] = pos;
+    meta[pos] = make_int2(a.rank, p);
+    a.srcrow[pos] = t;
+  }
+}
+
 // P1..P3 (all 256 threads of every CTA; cooperative grid).  Ends with a grid
 // barrier: the receive layout (dbase, slot_rows, need_src, ...) is then visible
 // to every CTA.  fsm: this CTA's dynamic shared memory (front layout).
@@ -825,6 +885,11 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
   const int bitem = s_item;
   TG_STAMP(8);
   const int ngroups = (a.T + kRouterRows - 1) / kRouterRows;
+  // world == 1, phased front: exchange + layout by every block from the chunk counts (the bases
+  // fit the router ring)
+  const bool lx = a.local_rows && a.world == 1 && ngroups > (int)VGRID / router_nkp(a.d, a.E_r) &&
+                  (size_t)((a.T + kRankBlock - 1) / kRankBlock + 2) * a.nkeys * 4 <=
+                      (size_t)router_nbuf(a.d, a.E_r, a.nkeys) * router_xtile_bytes(a.d, a.E_r);
   {
     const int nkp = router_nkp(a.d, a.E_r), KP = router_kpart(a.d, a.E_r);
     RouterSmem R;
@@ -851,48 +916,38 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
       // share its staged Wg slice), so the CTAs that start first — on the SMs the previous call's
       // tail frees first — run the whole router and its chain instead of waiting for the 64th CTA
       const int nitems = ngroups * nkp;
-      int item = bitem, cur_kp = -1;
-      if (a.E_r <= 32 && R.nbuf >= 2) {
-        // two Wg slices fit the slice region (rows [0, 32) and [32, 64)): the next item is claimed
-        // and its loads issued before this one computes
-        auto half = [&](int b) {
-          RouterSmem Rb = R;
-          Rb.wg = R.wg + (size_t)b * 32 * R.ldw;
-          return Rb;
-        };
-        int b = 0;
-        if (item < nitems) router_issue(a, half(0), item % ngroups, item / ngroups, 0, true);
-        while (item < nitems) {
-          if (threadIdx.x == 0) s_item = atomicAdd(a.gsync + 16 + a.cbuf, 1);
-          __syncthreads();
-          const int next = s_item;
-          if (next < nitems) {
-            router_issue(a, half(b ^ 1), next % ngroups, next / ngroups, b ^ 1, true);
-            cp_async_wait<1>();
-          } else {
-            cp_async_wait<0>();
-          }
-          __syncthreads();
-          const int grp = item % ngroups;
-          router_compute(a, half(b), grp, item / ngroups, b);
-          __syncthreads();
-          group_arrive(a, rk, grp, nkp, ngroups, reinterpret_cast<float *>(R.tail));
-          item = next;
-          b ^= 1;
-        }
-      }
+      // two Wg slices fit the slice region (E_r <= 32: rows [0, 32) and [32, 64)): the next item is
+      // claimed and its loads issued before this one computes; otherwise one buffer, the Wg slice
+      // restaged when the K part changes.  (One loop: router_compute is inlined once here.)
+      const bool two = a.E_r <= 32 && R.nbuf >= 2;
+      auto half = [&](int b) {
+        RouterSmem Rb = R;
+        Rb.wg = R.wg + (size_t)b * 32 * R.ldw;
+        return Rb;
+      };
+      int item = bitem, cur_kp = -1, b = 0;
+      if (two && item < nitems) router_issue(a, half(0), item % ngroups, item / ngroups, 0, true);
       while (item < nitems) {
         const int ikp = item / ngroups, grp = item % ngroups;
-        router_issue(a, R, grp, ikp, 0, ikp != cur_kp);
-        cur_kp = ikp;
+        if (!two) {
+          router_issue(a, R, grp, ikp, 0, ikp != cur_kp);
+          cur_kp = ikp;
+        }
         if (threadIdx.x == 0) s_item = atomicAdd(a.gsync + 16 + a.cbuf, 1);  // the next one, meanwhile
-        cp_async_wait<0>();
         __syncthreads();
         const int next = s_item;
-        router_compute(a, R, grp, ikp, 0);
+        if (two && next < nitems) {
+          router_issue(a, half(b ^ 1), next % ngroups, next / ngroups, b ^ 1, true);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncthreads();
+        router_compute(a, two ? half(b) : R, grp, ikp, b);
         __syncthreads();
         group_arrive(a, rk, grp, nkp, ngroups, reinterpret_cast<float *>(R.tail));
         item = next;
+        if (two) b ^= 1;
       }
     } else if (slot < bpp && slot < ngroups) {
       const int nit = (ngroups - slot + bpp - 1) / bpp;
@@ -948,7 +1003,10 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
       for (int ch = VBID; ch < nchunks; ch += VGRID) rank_chunk(a, ch, R.tail);
       TG_STAMP(13);
       grid_barrier_z(gbar, nbar++, a.err, a.ncta);
-      if (VBID == 0) {
+      if (lx) {
+        int32_t *base = reinterpret_cast<int32_t *>(R.xt);  // the router ring is free now
+        local_exchange_layout(a, nchunks, base, base + nchunks * a.nkeys, base + (nchunks + 1) * a.nkeys);
+      } else if (VBID == 0) {
         TG_STAMP(1);
         exchange_counts(a, nchunks, reinterpret_cast<int32_t *>(R.tail));
         TG_STAMP(14);
@@ -971,7 +1029,7 @@ __device__ __forceinline__ void front_phase(const CallArgs &a, const RouteKeys &
     grid_barrier_z(gbar, nbar++, a.err, a.ncta);
   }
   TG_STAMP(3);
-  if (a.local_rows && a.T * a.k > a.layout_block) {  // (smaller calls: by the exchange block)
+  if (!lx && a.local_rows && a.T * a.k > a.layout_block) {  // (smaller calls: by the exchange block)
     local_layout(a, VBID * blockDim.x + threadIdx.x, VGRID * blockDim.x);
     grid_barrier_z(gbar, nbar++, a.err, a.ncta);
   }
@@ -1066,25 +1124,32 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw, 
     }
   };
   const int total = npairs + nsh;
-  if (!claim) {
-    for (int p = w; p < total; p += nw) one(p);
-    return;
-  }
-  // early start: pairs claimed by whichever warps run first; the warp that completes the last
-  // pair releases the data flags (sync[3] counts completed pairs)
+  // static: pairs w, w + nw, ...; early start: chunks of kClaim pairs claimed by whichever warps
+  // run first, the warp that completes the last pair releasing the data flags (sync[3] counts
+  // completed pairs).  One loop, so the pair body is inlined once (cold code, once per call).
   constexpr int kClaim = 4;
+  int p = claim ? 0 : w, p1 = claim ? 0 : total;
+  const int step = claim ? 1 : nw;
   for (;;) {
-    int p0 = 0;
-    if (lane == 0) p0 = atomicAdd(claim, kClaim);
-    p0 = __shfl_sync(0xffffffffu, p0, 0);
-    if (p0 >= total) break;
-    const int p1 = min(p0 + kClaim, total);
-    for (int p = p0; p < p1; ++p) one(p);
-    __syncwarp();
-    if (lane == 0) {
-      fence_scope(a.world > 1);  // this warp's row / origin stores (peer memory) before the count
-      if (atomicAdd(a.sync + 3, p1 - p0) + (p1 - p0) == total) release_data_flags(a);
+    if (p >= p1) {
+      if (!claim) break;
+      if (p1 > 0) {  // this warp's claimed chunk is done
+        __syncwarp();
+        if (lane == 0) {
+          fence_scope(a.world > 1);  // its row / origin stores (peer memory) before the count
+          const int n = kClaim - max(0, p1 - total);
+          if (atomicAdd(a.sync + 3, n) + n == total) release_data_flags(a);
+        }
+      }
+      int p0 = 0;
+      if (lane == 0) p0 = atomicAdd(claim, kClaim);
+      p0 = __shfl_sync(0xffffffffu, p0, 0);
+      if (p0 >= total) break;
+      p = p0;
+      p1 = p0 + kClaim;
     }
+    if (p < total) one(p);
+    p += step;
   }
 }
 
@@ -1113,17 +1178,23 @@ __device__ __forceinline__ void dispatch_local_rows(const CallArgs &a, int w, in
     }
   };
   const int total = nrecv + nsh;
-  if (claim) {  // early start: rows claimed in receive order by whichever warps run first
-    constexpr int kClaim = 4;
-    for (;;) {
+  // static: rows w, w + nw, ...; early start: chunks claimed in receive order by whichever warps
+  // run first (one loop: the row body is inlined once)
+  constexpr int kClaim = 4;
+  int r = claim ? 0 : w, r1 = claim ? 0 : total;
+  const int step = claim ? 1 : nw;
+  for (;;) {
+    if (r >= r1) {
+      if (!claim) break;
       int r0 = 0;
       if (lane == 0) r0 = atomicAdd(claim, kClaim);
       r0 = __shfl_sync(0xffffffffu, r0, 0);
       if (r0 >= total) break;
-      for (int r = r0; r < min(r0 + kClaim, total); ++r) copy_one(r);
+      r = r0;
+      r1 = min(r0 + kClaim, total);
     }
-  } else {
-    for (int r = w; r < total; r += nw) copy_one(r);
+    copy_one(r);
+    r += step;
   }
 }
 
