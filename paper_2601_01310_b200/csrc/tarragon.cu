@@ -1052,6 +1052,10 @@ static tg_status host_path_init(tg_ctx *c) {
   if (c->wait32 && c->write32) {
     CK(cudaMalloc(&c->hk_dev, 8 * sizeof(int)));
     CK(cudaMemset(c->hk_dev, 0, 8 * sizeof(int)));
+    // the copy streams are non-blocking (no implicit order after the legacy stream's memset):
+    // the words must read zero before the first stream wait on them (a fresh allocation can hold
+    // stale values from memory freed earlier in the process)
+    CK(cudaDeviceSynchronize());
   }
   return TG_OK;
 }
