@@ -390,7 +390,7 @@ def main():
         L = wl.make_layer(shape, args.seed)
         x = wl.make_tokens(shape, args.seed, T=max(n, 1))
         times = []
-        nwarm = 1  # one untimed oracle sample (builds and pages in the oracle); bounded run time
+        nwarm = args.warmup  # untimed oracle samples of <= 4 tokens (page the oracle in); bounded run time
         for _ in range(nwarm):
             cpu_oracle_sample(shape, L, x, pl, min(n, 4), cores)
         for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
