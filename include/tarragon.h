@@ -241,7 +241,14 @@ tg_status tg_kv_restore(tg_ctx *ctx, void *dst, size_t bytes, size_t offset, voi
  * [n_tokens][d], must not alias x.  n_tokens <= max_tokens_per_rank (may be
  * 0).  Enqueued on `stream` (cudaStream_t; NULL = legacy default stream);
  * returns without synchronising.  x must stay valid until the stream passes
- * the call.                                                                */
+ * the call.  One kernel launch (programmatic dependent launch): consecutive
+ * calls on one stream overlap — the next call's CTAs start on the SMs the
+ * previous call frees and, for decode-sized calls, begin their expert GEMM
+ * before the previous call has completed (alternate calls use alternate
+ * internal buffer sets).  Stream order still holds for the caller: work
+ * enqueued after a call sees its output.  The launch keeps one CTA per SM
+ * and never waits on a later call, so every CTA becomes resident; do not run
+ * a kernel beside it on the same GPU that waits for the layer.           */
 tg_status tg_moe_layer(tg_ctx *ctx, const void *x, void *out, int n_tokens, void *stream);
 
 /* End-to-end form: x_host/out_host are pinned HOST buffers.  The H2D copy of
