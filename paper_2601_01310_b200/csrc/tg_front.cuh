@@ -1128,28 +1128,28 @@ __device__ __forceinline__ void dispatch_rows(const CallArgs &a, int w, int nw, 
   // run first, the warp that completes the last pair releasing the data flags (sync[3] counts
   // completed pairs).  One loop, so the pair body is inlined once (cold code, once per call).
   constexpr int kClaim = 4;
-  int p = claim ? 0 : w, p1 = claim ? 0 : total;
+  int p = claim ? 0 : w, p1 = claim ? 0 : total, done = 0;
   const int step = claim ? 1 : nw;
   for (;;) {
     if (p >= p1) {
       if (!claim) break;
-      if (p1 > 0) {  // this warp's claimed chunk is done
-        __syncwarp();
-        if (lane == 0) {
-          fence_scope(a.world > 1);  // its row / origin stores (peer memory) before the count
-          const int n = kClaim - max(0, p1 - total);
-          if (atomicAdd(a.sync + 3, n) + n == total) release_data_flags(a);
-        }
-      }
       int p0 = 0;
       if (lane == 0) p0 = atomicAdd(claim, kClaim);
       p0 = __shfl_sync(0xffffffffu, p0, 0);
       if (p0 >= total) break;
       p = p0;
       p1 = p0 + kClaim;
+      done += min(p1, total) - p0;
     }
     if (p < total) one(p);
     p += step;
+  }
+  if (claim && done > 0) {  // one fence per warp, after all its claims: its stores before the count
+    __syncwarp();
+    if (lane == 0) {
+      fence_scope(a.world > 1);
+      if (atomicAdd(a.sync + 3, done) + done == total) release_data_flags(a);
+    }
   }
 }
 
