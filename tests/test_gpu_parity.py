@@ -214,7 +214,7 @@ def test_host_entry_point_e2e(cfg, ncalls):
     od = _run(layer, x)
     assert torch.equal(oh.view(torch.int16), od.cpu().view(torch.int16))
     # pipelined calls over the two staging buffers, different inputs (and sizes) per call
-    sizes = [sh.T, max(sh.T - 3, 1), max(sh.T // 2, 1), 1, sh.T]
+    sizes = [sh.T, max(sh.T - 3, 1), max(sh.T // 2, 1), 1, 0, sh.T]  # (0: a call with no tokens)
     xs = [wl.make_tokens(sh, 2000 + i, sizes[i % len(sizes)]).pin_memory() for i in range(ncalls)]
     ohs = [torch.empty_like(v).pin_memory() for v in xs]
     for v, o in zip(xs, ohs):
