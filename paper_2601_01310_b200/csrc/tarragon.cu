@@ -776,6 +776,10 @@ static CallArgs call_args(tg_ctx *c, int T, const void *x, void *out, RouteKeys 
     // arrivals and the sources' waits must take the same branch.
     const long arrivals = (long)c->T_max * c->k * ((c->d + 2 * BM - 1) / (2 * BM));
     a.tok_comb = comb && (c->world == 1 || arrivals <= kTokCombMaxArrivals) ? 1 : 0;
+    // prefill-sized calls interleave GEMM2 into the work list (H consumed while in L2)
+    a.g2lag = (T * c->k >= 8192) ? 8 : 0;  // same-box A/B, Qwen-shaped prefill: lag 0 888, 2 904, 4 876, 8 874 us
+    const char *gl = getenv("TG_G2LAG");  // development override (A/B timing)
+    if (gl) a.g2lag = atoi(gl);
     const char *lb = getenv("TG_LAYOUT");  // development override (A/B timing)
     a.layout_block = lb ? atoi(lb) : kLocalLayoutBlock;
     const char *dv = getenv("TG_DEV");

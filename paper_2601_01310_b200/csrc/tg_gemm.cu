@@ -31,6 +31,7 @@
 namespace tg {
 
 constexpr int kMaxPlan = kMaxSlotsPerRank + 2;
+constexpr int kMaxG2Lag = 16;
 
 struct GemmShared {
   uint64_t full[kStages];
@@ -54,6 +55,7 @@ struct GemmShared {
   int g2off[kMaxPlan];     // GEMM2 unit offsets
   int goff[kMaxPlan];      // dependency-group offsets
   int roff[kMaxPlan];      // reduction-group offsets
+  int boff[kMaxPlan + kMaxG2Lag];  // interleaved order (g2lag > 0): block j = GEMM1 of slot j, GEMM2 of slot j - lag
 };
 
 // silu(a) = a / (1 + e^-a) with the fast exp (ex2.approx of a * log2 e: relative error <= 2 +
@@ -192,6 +194,7 @@ __device__ void build_plan(const CallArgs &a, GemmShared *P) {
     bg += nt;
     bred += (ns > 1) ? nt * ctiles : 0;
   }
+  __syncwarp();  // every lane's offsets written
   if (lane == 31) {
     P->nrecv = br;  // after the scan loop: every routed slot's rows
     P->stage_bytes = 2 * kTileBytes + nbw * BK * 2;  // multiple of 2 KB: 1 KB swizzle-atom aligned
@@ -203,6 +206,19 @@ __device__ void build_plan(const CallArgs &a, GemmShared *P) {
     P->NS = NS;
     P->G1 = bu1;
     P->total = bu1 + bu2;
+    // GEMM2 units of slot s queued right after the GEMM1 units of slot s + lag (their H tiles
+    // still in L2) instead of after every GEMM1 unit; each G2 unit's dependencies stay earlier in
+    // the queue.  Order only: every unit's arithmetic is unchanged.
+    const int L = min(a.g2lag, kMaxG2Lag);
+    if (L > 0) {
+      int acc = 0;
+      for (int j = 0; j < NS + L; ++j) {
+        P->boff[j] = acc;
+        if (j < NS) acc += P->g1off[j + 1] - P->g1off[j];
+        if (j >= L) acc += P->g2off[j - L + 1] - P->g2off[j - L];
+      }
+      P->boff[NS + L] = acc;
+    }
     P->ngroups = bg;
     if (VBID == 0) *a.n_units = bu1 + bu2;
     if (bg + bred > a.n_ctr_max) {  // capacity guard (sized at init for the worst case)
@@ -228,10 +244,23 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
   Unit U;
   const int S = a.S_loc, NS = P->NS;
   const int ftiles = (a.F + BM - 1) / BM;
-  if (u < P->G1) {
-    const int s = find_seg(P->g1off, NS, u);
+  const int L = min(a.g2lag, kMaxG2Lag);
+  int u1 = -1, u2i = -1;  // index among the GEMM1 / GEMM2 units
+  if (L > 0) {
+    const int j = find_seg(P->boff, NS + L, u);
+    const int loc = u - P->boff[j];
+    const int n1 = (j < NS) ? P->g1off[j + 1] - P->g1off[j] : 0;
+    if (loc < n1) u1 = P->g1off[j] + loc;
+    else u2i = P->g2off[j - L] + (loc - n1);
+  } else if (u < P->G1) {
+    u1 = u;
+  } else {
+    u2i = u - P->G1;
+  }
+  if (u1 >= 0) {
+    const int s = find_seg(P->g1off, NS, u1);
     const bool sh = (s == S);
-    const int loc = u - P->g1off[s];
+    const int loc = u1 - P->g1off[s];
     const int f = loc / P->nt[s], n = loc % P->nt[s];
     U.kind = sh ? U_G1_SH : U_G1;
     U.slot = sh ? 0 : s;
@@ -248,7 +277,7 @@ __device__ __forceinline__ Unit decode_unit(const CallArgs &a, const GemmShared 
     U.ntiles = P->nt[s];
     U.dual = 0;
   } else {
-    const int u2 = u - P->G1;
+    const int u2 = u2i;
     const int s = find_seg(P->g2off, NS, u2);
     const bool sh = (s == S);
     const int ns = sh ? 1 : a.nsplit;

@@ -156,6 +156,7 @@ struct CallArgs {
   int local_rows;        // world == 1: rows copied in row order beside the GEMM, per-tile counters
   int layout_block;      // world == 1: pairs up to which the exchange block lays out the call (decode)
   int tok_comb;          // per-token arrival counters, combine without a grid barrier (not in replays)
+  int g2lag;             // GEMM2 units of slot s queued after the GEMM1 units of slot s + g2lag (0: after all GEMM1)
   // host-buffer path (tg_moe_layer_host): device words shared with the copy streams, which order
   // themselves with stream memory operations so no stream op sits between consecutive kernels
   // (the PDL overlap); null otherwise.  [0,1] x staged, [2,3] out drained, [4,5] exit counts,
